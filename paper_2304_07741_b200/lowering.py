@@ -1,0 +1,1064 @@
+"""Lowering: concrete kernel graph -> fused device-kernel plan (+ its adjoint).
+
+This is the host half of the hot path (SURVEY §3.4 "new build", §7 decisions
+2-3).  Given a :class:`~paper_2304_07741_b200.graph.ConcreteGraph` it decides
+
+* which node values are **materialised** in HBM.  Only reductions and
+  contractions are: Fold, Softmax, FC outputs, plus the kernel output.  Every
+  rearrangement (Group/Shift/Unfold) and every pointwise op (ew, bcast) is
+  *inlined* into the loads of its consumer as index arithmetic + zero
+  predicates (north star: "rearrangement primitives are never materialised");
+* the backward schedule: the adjoint of every primitive is a *pull* (gather)
+  expression — col2im-as-gather for Unfold, replica sums for Broadcast LHS,
+  tie-split for max/min — so no atomics are needed and results are
+  bitwise deterministic (SURVEY §7 decision 5);
+* the device kernels: each materialised tensor is produced by one launch of a
+  hand-written template from ``csrc/kernels/canvas_kernels.cuh``
+  (``pointwise``, ``gemm_nk``, ``gemm_wgrad``/``reduce_partials``), instantiated
+  with a *functor* this module emits — straight-line C++ that evaluates the
+  node's producer chain at one coordinate with compile-time extents (so every
+  index div/mod is a multiply-shift).
+
+The result is a :class:`Plan` whose ``blob()`` is the flat POD payload the
+C-ABI ``canvas_plan_create`` consumes (include/canvas_b200.h).
+
+Numeric conventions: unfold U[..k..,h] = I[.., h+k-K//2] zero
+padded, per-stage predicates (A.3); shift out[h] = in[h+off] (A.2); bcast tile
+order lhs index = r mod L, ``sub`` = lhs - rhs, min/max ties split 1/2 (A.8);
+fold max ties split evenly (A.6); relu'(0) = abs'(0) = 0 (A.5); softmax
+max-subtracted (A.7); FC dense, bias-free, W[out, prod(in ch)] (A.4).
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+from dataclasses import dataclass, field
+
+from .graph import VIEW_OPS, ConcreteGraph, LoweringError
+
+ABI_VERSION = 1
+BLOB_MAGIC = b"CNVSBLOB"
+MAX_KSLOTS = 24  # pointers per kernel argument block (csrc/kernels/canvas_kernels.cuh)
+
+# fixed global slots; weights / grads / saved / workspace follow (see Plan.slot_*)
+SLOT_X, SLOT_Y, SLOT_DY, SLOT_DX = 0, 1, 2, 3
+
+# beta policies for stores into caller-visible outputs shared by the r copies (Fig.-2)
+BETA_NONE, BETA_AFTER_FIRST, BETA_ALWAYS = 0, 1, 2
+
+POINTWISE_BLOCK = 256
+POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
+GEMM_TILE = 64
+SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
+
+
+@dataclass
+class TDesc:
+    """Where a tensor lives: global slot + strides (elements).  ``dims`` are
+    the node extents; ``strides`` per dim; ``bstride`` per image."""
+
+    slot: int
+    bstride: int
+    strides: tuple
+    dims: tuple
+
+
+@dataclass
+class SizeRule:
+    """bytes(N) = ceil(N * a_num / a_den) + b."""
+
+    a_num: int
+    a_den: int
+    b: int
+
+    def eval(self, n: int) -> int:
+        return -(-n * self.a_num // self.a_den) + self.b
+
+
+@dataclass
+class GridRule:
+    """g = min(ceil((a*N + b) / d), cap) (cap 0 = none)."""
+
+    a: int
+    b: int
+    d: int
+    cap: int = 0
+
+    def eval(self, n: int) -> int:
+        g = -(-(self.a * n + self.b) // self.d)
+        return min(g, self.cap) if self.cap else g
+
+
+@dataclass
+class Launch:
+    kind: str  # "kernel" | "memset"
+    phase: int  # 0 forward, 1 backward
+    name: str = ""
+    kernel: int = -1
+    block: int = 256
+    grid: tuple = ()
+    slots: tuple = ()
+    beta: int = BETA_NONE
+    memset_slot: int = -1
+    memset_size: SizeRule | None = None
+    what: str = ""  # human-readable role (profiles / DESIGN tables)
+    bytes_per_image: int = 0  # algorithmic HBM bytes per image (roofline)
+    flops_per_image: int = 0  # useful FLOPs per image (2 per MAC)
+
+
+@dataclass
+class Plan:
+    graph: ConcreteGraph
+    c_in: int
+    c_out: int
+    stride: int
+    h_in: int
+    w_in: int
+    copies: int
+    mode: str  # "concat" (C_out = r C_in) or "sum" (C_in = r C_out)
+    source: str = ""
+    kernel_names: list = field(default_factory=list)
+    launches: list = field(default_factory=list)
+    saved: list = field(default_factory=list)  # SizeRule per saved slot (one copy)
+    ws: list = field(default_factory=list)  # SizeRule per workspace slot
+    x_copy_off: int = 0
+    y_copy_off: int = 0
+    dx_copy_off: int = 0
+    dy_copy_off: int = 0
+    fwd_mat: dict = field(default_factory=dict)  # node -> TDesc of its forward value
+    notes: list = field(default_factory=list)
+
+    @property
+    def n_fc(self) -> int:
+        return len(self.graph.fc_nodes)
+
+    def slot_w(self, i: int) -> int:
+        return 4 + i
+
+    def slot_dw(self, i: int) -> int:
+        return 4 + self.n_fc + i
+
+    def slot_saved(self, k: int) -> int:
+        return 4 + 2 * self.n_fc + k
+
+    def slot_ws(self, k: int) -> int:
+        return 4 + 2 * self.n_fc + len(self.saved) + k
+
+    # -- C-ABI payload ---------------------------------------------------------------
+    def blob(self) -> bytes:
+        """Flat little-endian payload parsed by csrc/canvas_runtime.cpp (format v1).
+
+        header: magic[8], then int64s: version, n_kernels, n_launches, n_saved,
+        n_ws, n_fc, copies, x_copy_off, y_copy_off, dx_copy_off, dy_copy_off,
+        src_len, names_len; then (a_num, a_den, b) per saved and per ws slot;
+        then per launch: kind, phase, kernel, block, 3x(a,b,d,cap), nslots,
+        slots[MAX_KSLOTS], beta, memset_slot, memset (a_num,a_den,b); then the
+        CUDA source and the NUL-separated kernel names.
+        """
+        names = b"\0".join(n.encode() for n in self.kernel_names) + b"\0"
+        src = self.source.encode()
+        q = struct.Struct("<q")
+        out = bytearray(BLOB_MAGIC)
+        hdr = [ABI_VERSION, len(self.kernel_names), len(self.launches), len(self.saved), len(self.ws), self.n_fc, self.copies, self.x_copy_off, self.y_copy_off, self.dx_copy_off, self.dy_copy_off, len(src), len(names)]
+        for v in hdr:
+            out += q.pack(v)
+        for r in self.saved + self.ws:
+            out += struct.pack("<3q", r.a_num, r.a_den, r.b)
+        for L in self.launches:
+            grid = list(L.grid) if L.grid else [GridRule(0, 1, 1)] * 3
+            slots = list(L.slots) + [-1] * (MAX_KSLOTS - len(L.slots))
+            ms = L.memset_size or SizeRule(0, 1, 0)
+            out += struct.pack("<4q", 0 if L.kind == "kernel" else 1, L.phase, L.kernel, L.block)
+            for g in grid:
+                out += struct.pack("<4q", g.a, g.b, g.d, g.cap)
+            out += struct.pack("<q", len(L.slots))
+            out += struct.pack(f"<{MAX_KSLOTS}q", *slots)
+            out += struct.pack("<5q", L.beta, L.memset_slot, ms.a_num, ms.a_den, ms.b)
+        out += src + names
+        return bytes(out)
+
+    # -- helpers used by module / bench ------------------------------------------------
+    def sizes(self, n: int) -> tuple[int, int, int]:
+        """(saved bytes for all copies, workspace bytes, fwd workspace bytes) at batch n."""
+        al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+        saved = sum(al(r.eval(n)) for r in self.saved) * self.copies
+        ws = sum(al(r.eval(n)) for r in self.ws)
+        return saved, ws, 0
+
+
+# ====================================================================================
+# Code emission
+# ====================================================================================
+
+_EW_FWD = {
+    "relu": "fmaxf({0}, 0.f)",
+    "abs": "fabsf({0})",
+    "sin": "sinf({0})",
+    "exp": "expf({0})",
+    "neg": "(-{0})",
+}
+_BC_FWD = {
+    "add": "({0} + {1})",
+    "sub": "({0} - {1})",
+    "mul": "({0} * {1})",
+    "min": "fminf({0}, {1})",
+    "max": "fmaxf({0}, {1})",
+}
+
+
+class Fn:
+    """Straight-line code for one functor body with memoised coordinates/values.
+
+    Coordinates are C ``int`` expressions; the memo keys on their text, so a
+    coordinate reached twice (diamonds, shared prefixes) is computed once
+    (common-subexpression elimination at emission time)."""
+
+    def __init__(self, lw: "Lowerer", indent: int = 2):
+        self.lw = lw
+        self.lines: list[str] = []
+        self.scopes: list[dict] = [{}]
+        self.indent = indent
+        self.k = 0
+        self.local_slots: list[int] = []
+        self.bases: dict = {}
+
+    # -- bookkeeping -----------------------------------------------------------
+    def emit(self, s: str) -> None:
+        self.lines.append("  " * self.indent + s)
+
+    def fresh(self, p: str) -> str:
+        self.k += 1
+        return f"{p}{self.k}"
+
+    def memo_get(self, key):
+        for sc in reversed(self.scopes):
+            if key in sc:
+                return sc[key]
+        return None
+
+    def memo_put(self, key, val) -> None:
+        self.scopes[-1][key] = val
+
+    def open(self, head: str) -> None:
+        self.emit(head + " {")
+        self.indent += 1
+        self.scopes.append({})
+
+    def close(self) -> None:
+        self.scopes.pop()
+        self.indent -= 1
+        self.emit("}")
+
+    def ivar(self, expr: str) -> str:
+        expr = str(expr)
+        if expr.lstrip("-").isdigit() or expr.isidentifier():
+            return expr
+        got = self.memo_get(("i", expr))
+        if got:
+            return got
+        v = self.fresh("i")
+        self.emit(f"const int {v} = {expr};")
+        self.memo_put(("i", expr), v)
+        return v
+
+    def fvar(self, expr: str, key=None) -> str:
+        key = key or ("f", expr)
+        got = self.memo_get(key)
+        if got:
+            return got
+        v = self.fresh("v")
+        self.emit(f"const float {v} = {expr};")
+        self.memo_put(key, v)
+        return v
+
+    def ptr(self, slot: int) -> str:
+        if slot not in self.local_slots:
+            if len(self.local_slots) >= MAX_KSLOTS:
+                raise LoweringError("kernel needs too many tensors")
+            self.local_slots.append(slot)
+        return f"a.p[{self.local_slots.index(slot)}]"
+
+    def base(self, d: TDesc) -> str:
+        """Per-image base pointer of a tensor (``n`` is the image index)."""
+        key = (d.slot, d.bstride)
+        if key in self.bases:
+            return self.bases[key]
+        b = self.fresh("b")
+        self.bases[key] = b
+        # hoisted: emitted into the preamble (before any scope) by the caller
+        self.pre.append(f"float* __restrict__ {b} = {self.ptr(d.slot)} + n * {d.bstride}LL;")
+        return b
+
+    def offset(self, d: TDesc, coords) -> str:
+        terms = [f"{c}*{s}" if s != 1 else f"{c}" for c, s in zip(coords, d.strides) if s != 0 and c != "0"]
+        return self.ivar(" + ".join(terms) if terms else "0")
+
+    def load(self, d: TDesc, coords) -> str:
+        off = self.offset(d, coords)
+        return self.fvar(f"__ldg({self.base(d)} + {off})")
+
+    def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
+        off = self.offset(d, coords)
+        b = self.base(d)
+        if beta:
+            self.emit(f"if (a.beta) {b}[{off}] += {val}; else {b}[{off}] = {val};")
+        else:
+            self.emit(f"{b}[{off}] = {val};")
+
+    def decompose(self, flat: str, ext) -> list[str]:
+        """Row-major flat index -> coordinates (constant divisors)."""
+        coords = [None] * len(ext)
+        rest = flat
+        for i in range(len(ext) - 1, -1, -1):
+            e = ext[i]
+            if i == 0:
+                coords[0] = self.ivar(rest) if e > 1 else "0"
+            elif e == 1:
+                coords[i] = "0"
+            else:
+                coords[i] = self.ivar(f"{rest} % {e}")
+                rest = self.ivar(f"{rest} / {e}")
+        return coords
+
+    def flatten(self, coords, ext) -> str:
+        expr = None
+        for c, e in zip(coords, ext):
+            expr = c if expr is None else f"({expr})*{e} + {c}"
+        return self.ivar(expr if expr is not None else "0")
+
+
+class Lowerer:
+    """Builds a :class:`Plan` for one concrete graph and replacement target."""
+
+    def __init__(self, g: ConcreteGraph, plan: Plan):
+        self.g = g
+        self.p = plan
+        self.nodes = g.nodes
+        self.out = g.output
+        self.kernels: list[str] = []  # functor + kernel source per kernel
+        # forward materialisation: reductions, contractions, input, output (module docstring)
+        self.fwd_mat = {0} | {v.id for v in self.nodes if v.op in ("fold", "softmax", "fc")} | {self.out}
+        # gradients materialised in the backward: every non-view node except the
+        # output (its gradient is dy) — views pull through gathers
+        self.grad_mat = {0} | {v.id for v in self.nodes if v.op not in VIEW_OPS and v.id != self.out and v.op != "input"}
+        self.fwd_desc: dict[int, TDesc] = {}
+        self.count_desc: dict[int, TDesc] = {}
+        self.grad_desc: dict[int, TDesc] = {}
+        self.dgrad_desc: dict[int, TDesc] = {}  # FC node u -> contribution buffer for its input
+        self.dot_desc: dict[int, TDesc] = {}  # softmax node u -> row dot buffer
+        self.computing_grad = None
+
+    # -------------------------------------------------------------- descriptors
+    @staticmethod
+    def _contig(ext) -> tuple:
+        st, acc = [], 1
+        for e in reversed(ext):
+            st.append(acc)
+            acc *= e
+        return tuple(reversed(st))
+
+    def _new_saved(self, ext) -> TDesc:
+        n = math.prod(ext)
+        self.p.saved.append(SizeRule(4 * n, 1, 0))
+        return TDesc(self.p.slot_saved(len(self.p.saved) - 1), n, self._contig(ext), tuple(ext))
+
+    def _new_ws(self, ext) -> tuple[int, TDesc]:
+        n = math.prod(ext)
+        self.p.ws.append(SizeRule(4 * n, 1, 0))
+        k = len(self.p.ws) - 1
+        return k, TDesc(-1 - k, n, self._contig(ext), tuple(ext))  # slot fixed up in finish()
+
+    def x_desc(self) -> TDesc:
+        p, n0 = self.p, self.nodes[0]
+        c, h, w = n0.ext
+        s = p.stride
+        ctot = p.c_in
+        return TDesc(SLOT_X, ctot * p.h_in * p.w_in, (p.h_in * p.w_in, s * p.w_in, s), (c, h, w))
+
+    def dx_desc(self) -> TDesc:
+        d = self.x_desc()
+        return TDesc(SLOT_DX, d.bstride, d.strides, d.dims)
+
+    def y_desc(self, slot=SLOT_Y) -> TDesc:
+        c, h, w = self.nodes[self.out].ext
+        ctot = self.p.c_out
+        return TDesc(slot, ctot * h * w, (h * w, w, 1), (c, h, w))
+
+    # -------------------------------------------------------------- forward values
+    def val(self, f: Fn, v: int, coords: tuple) -> str:
+        key = ("val", v, coords)
+        got = f.memo_get(key)
+        if got:
+            return got
+        if v in self.fwd_desc and v != getattr(f, "computing", None):
+            r = f.load(self.fwd_desc[v], coords)
+        else:
+            r = self.compute(f, v, coords)
+        f.memo_put(key, r)
+        return r
+
+    def compute(self, f: Fn, v: int, coords: tuple) -> str:
+        nd = self.nodes[v]
+        op, at = nd.op, nd.attr
+        if op == "group":
+            d, b = at["dim"], at["B"]
+            merged = f.ivar(f"{coords[d]}*{b} + {coords[d + 1]}" if coords[d] != "0" else coords[d + 1])
+            return self.val(f, nd.ins[0], coords[:d] + (merged,) + coords[d + 2 :])
+        if op == "shift":
+            ax, off = at["ax"], at["off"]
+            e = nd.ext[ax]
+            src = f.ivar(f"{coords[ax]} + ({off})")
+            pred = f"((unsigned){src} < {e}u)"
+            cl = f.ivar(f"min(max({src}, 0), {e - 1})")
+            inner = self.val(f, nd.ins[0], coords[:ax] + (cl,) + coords[ax + 1 :])
+            return f.fvar(f"{pred} ? {inner} : 0.f")
+        if op == "unfold":
+            k_at, K, ax_out = at["at"], at["K"], at["ax_out"]
+            e = nd.ext[ax_out]
+            src = f.ivar(f"{coords[ax_out]} + {coords[k_at]} - {K // 2}")
+            pred = f"((unsigned){src} < {e}u)"
+            cl = f.ivar(f"min(max({src}, 0), {e - 1})")
+            c2 = list(coords)
+            c2[ax_out] = cl
+            del c2[k_at]
+            inner = self.val(f, nd.ins[0], tuple(c2))
+            return f.fvar(f"{pred} ? {inner} : 0.f")
+        if op == "ew":
+            x = self.val(f, nd.ins[0], coords)
+            return f.fvar(_EW_FWD[at["fn"]].format(x))
+        if op == "bcast":
+            lhs = self.val(f, nd.ins[0], self.lhs_coords(f, nd, coords))
+            rhs = self.val(f, nd.ins[1], coords)
+            return f.fvar(_BC_FWD[at["op"]].format(lhs, rhs))
+        raise LoweringError(f"node {v} ({op}) must be materialised before it is read")
+
+    def lhs_coords(self, f: Fn, nd, coords) -> tuple:
+        at = nd.attr
+        cs, nl, nr, L = at["cs"], at["nl"], at["nr"], at["L"]
+        core = coords[cs : cs + nr]
+        if nl == 0:
+            lc = ()
+        elif at["M"] == 1 and tuple(at["lcore"]) == tuple(at["rcore"]):
+            lc = core
+        else:
+            r = f.flatten(core, at["rcore"])
+            l = f.ivar(f"{r} % {L}") if at["M"] > 1 else r
+            lc = tuple(f.decompose(l, at["lcore"]))
+        return coords[:cs] + lc + coords[cs + nr :]
+
+    # -------------------------------------------------------------- gradients
+    def grad(self, f: Fn, v: int, coords: tuple) -> str:
+        key = ("grad", v, coords)
+        got = f.memo_get(key)
+        if got:
+            return got
+        if v == self.out:
+            r = f.load(self.dy_desc, coords)
+        elif v in self.grad_desc and v != self.computing_grad:
+            r = f.load(self.grad_desc[v], coords)
+        else:
+            r = self.grad_sum(f, v, coords)
+        f.memo_put(key, r)
+        return r
+
+    def grad_sum(self, f: Fn, v: int, coords: tuple) -> str:
+        terms = [self.contrib(f, u, pos, v, coords) for u, pos in self.nodes[v].consumers]
+        terms = [t for t in terms if t != "0.f"]
+        if not terms:
+            return "0.f"
+        return f.fvar(" + ".join(terms)) if len(terms) > 1 else terms[0]
+
+    def contrib(self, f: Fn, u: int, pos: int, v: int, coords: tuple) -> str:
+        """Contribution of edge v -(pos)-> u to dL/dv at ``coords`` (pull form)."""
+        nu = self.nodes[u]
+        op, at = nu.op, nu.attr
+        if op == "group":
+            d, b = at["dim"], at["B"]
+            c = coords[d]
+            hi, lo = f.ivar(f"{c} / {b}"), f.ivar(f"{c} % {b}")
+            return self.grad(f, u, coords[:d] + (hi, lo) + coords[d + 1 :])
+        if op == "shift":
+            ax, off = at["ax"], at["off"]
+            e = nu.ext[ax]
+            src = f.ivar(f"{coords[ax]} - ({off})")
+            cl = f.ivar(f"min(max({src}, 0), {e - 1})")
+            g = self.grad(f, u, coords[:ax] + (cl,) + coords[ax + 1 :])
+            return f.fvar(f"((unsigned){src} < {e}u) ? {g} : 0.f")
+        if op == "unfold":
+            # col2im as a gather: dI[h] = sum_k dU[k, h - k + K//2] (valid terms only)
+            k_at, K, ax_in = at["at"], at["K"], at["ax_in"]
+            e = nu.ext[at["ax_out"]]
+            terms = []
+            for k in range(K):
+                src = f.ivar(f"{coords[ax_in]} - ({k - K // 2})")
+                cl = f.ivar(f"min(max({src}, 0), {e - 1})")
+                c2 = list(coords)
+                c2[ax_in] = cl
+                c2.insert(k_at, str(k))
+                g = self.grad(f, u, tuple(c2))
+                terms.append(f"(((unsigned){src} < {e}u) ? {g} : 0.f)")
+            return f.fvar(" + ".join(terms))
+        if op == "ew":
+            g = self.grad(f, u, coords)
+            x = self.val(f, v, coords)
+            fn = at["fn"]
+            if fn == "relu":
+                return f.fvar(f"{x} > 0.f ? {g} : 0.f")
+            if fn == "abs":
+                return f.fvar(f"{x} > 0.f ? {g} : ({x} < 0.f ? -{g} : 0.f)")
+            if fn == "sin":
+                return f.fvar(f"{g} * cosf({x})")
+            if fn == "exp":
+                return f.fvar(f"{g} * expf({x})")
+            if fn == "neg":
+                return f.fvar(f"-{g}")
+        if op == "fold":
+            dim, D = at["dim"], at["D"]
+            uc = coords[:dim] + coords[dim + 1 :]
+            g = self.grad(f, u, uc)
+            if at["mode"] == "avg":
+                return f.fvar(f"{g} / {float(D)!r}f")
+            m = self.val(f, u, uc)
+            cnt = f.load(self.count_desc[u], uc)
+            x = self.val(f, v, coords)
+            return f.fvar(f"{x} == {m} ? {g} / {cnt} : 0.f")
+        if op == "softmax":
+            y = self.val(f, u, coords)
+            g = self.grad(f, u, coords)
+            d = self.dot_desc[u]
+            rc = self.softmax_row_coords(nu, coords)
+            dot = f.load(d, rc)
+            return f.fvar(f"{y} * ({g} - {dot})")
+        if op == "fc":
+            return f.load(self.dgrad_desc[u], coords)
+        if op == "bcast":
+            return self.bcast_contrib(f, nu, pos, v, coords)
+        raise LoweringError(f"no adjoint for {op}")
+
+    def bcast_contrib(self, f: Fn, nu, pos: int, v: int, coords: tuple) -> str:
+        at = nu.attr
+        u = nu.id
+        lhs_n, rhs_n = nu.ins
+        bop = at["op"]
+        total = []
+        if pos == 1:  # v is the RHS: elementwise
+            g = self.grad(f, u, coords)
+            l = self.val(f, lhs_n, self.lhs_coords(f, nu, coords))
+            r = self.val(f, rhs_n, coords)
+            total.append(f.fvar(_bc_d_rhs(bop, g, l, r)))
+        else:  # v is the LHS: sum over the M replicas r = m*L + l
+            cs, nl, nr, L, M = at["cs"], at["nl"], at["nr"], at["L"], at["M"]
+            lcore = coords[cs : cs + nl]
+            lflat = f.flatten(lcore, at["lcore"]) if nl else "0"
+            l = self.val(f, lhs_n, coords) if bop in ("mul", "min", "max") else None
+
+            def term(mexpr: str) -> str:
+                rr = f.ivar(f"{mexpr}*{L} + {lflat}" if mexpr != "0" else lflat)
+                rc = coords[:cs] + tuple(f.decompose(rr, at["rcore"])) + coords[cs + nl :]
+                g = self.grad(f, u, rc)
+                r = self.val(f, rhs_n, rc) if bop in ("mul", "min", "max") else None
+                return f.fvar(_bc_d_lhs(bop, g, l, r))
+
+            if M == 1:
+                total.append(term("0"))
+            elif M <= 4:
+                total.append(f.fvar(" + ".join(term(str(m)) for m in range(M))))
+            else:
+                acc = f.fresh("s")
+                f.emit(f"float {acc} = 0.f;")
+                mv = f.fresh("m")
+                f.open(f"for (int {mv} = 0; {mv} < {M}; ++{mv})")
+                t = term(mv)
+                f.emit(f"{acc} += {t};")
+                f.close()
+                total.append(acc)
+        return total[0] if len(total) == 1 else f.fvar(" + ".join(total))
+
+    # -------------------------------------------------------------- softmax rows
+    @staticmethod
+    def softmax_geom(nd) -> tuple:
+        s, e = nd.attr["start"], nd.attr["end"]
+        pre = nd.ext[:s]
+        span = nd.ext[s : e + 1]
+        post = nd.ext[e + 1 :]
+        return pre, span, post
+
+    def softmax_row_coords(self, nd, coords) -> tuple:
+        s, e = nd.attr["start"], nd.attr["end"]
+        return coords[:s] + coords[e + 1 :]
+
+    # -------------------------------------------------------------- kernels
+    def add_kernel(self, name: str, functor: str, launcher: str) -> int:
+        self.kernels.append(functor + launcher)
+        self.p.kernel_names.append(name)
+        return len(self.p.kernel_names) - 1
+
+    def functor_pointwise(self, name: str, per_image: int, body_fn) -> tuple[str, list]:
+        """Functor for ``canvas::pointwise``: one output element (or row) per call."""
+        f = Fn(self)
+        f.pre = []
+        f.computing = None
+        body_fn(f)
+        src = [f"struct {name}_F {{", f"  static constexpr long long PER = {per_image}LL;", "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int r) {"]
+        src += ["    " + s for s in f.pre]
+        src += f.lines
+        src += ["  }", "};"]
+        return "\n".join(src) + "\n", f.local_slots
+
+    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0):
+        functor, slots = self.functor_pointwise(name, per_image, body_fn)
+        launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F>(a); }}\n'
+        k = self.add_kernel(name, functor, launcher)
+        grid = (GridRule(per_image, 0, POINTWISE_BLOCK, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        self.p.launches.append(Launch("kernel", phase, name, k, POINTWISE_BLOCK, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+
+    # ---- forward
+    def fwd_targets(self, v: int) -> list:
+        """[(TDesc, beta?)] every store of node v's forward value goes to."""
+        if v == self.out:
+            t = [(self.y_desc(), self.p.mode == "sum")]
+            if self.out in self.fwd_desc:  # also needed by its own adjoint
+                t.append((self.fwd_desc[v], False))
+            return t
+        return [(self.fwd_desc[v], False)]
+
+    def lower_forward(self) -> None:
+        g = self.g
+        out = self.nodes[self.out]
+        # descriptors of materialised forward values (reads)
+        self.fwd_desc[0] = self.x_desc()
+        for v in sorted(self.fwd_mat - {0}):
+            nd = self.nodes[v]
+            if v == self.out and not (nd.op == "softmax" or (nd.op == "fold" and nd.attr["mode"] == "max")):
+                continue  # output value never read back
+            self.fwd_desc[v] = self._new_saved(nd.ext)
+        for v in sorted(self.fwd_mat - {0}):
+            nd = self.nodes[v]
+            if nd.op == "fold" and nd.attr["mode"] == "max":
+                self.count_desc[v] = self._new_saved(nd.ext)
+        beta_y = BETA_AFTER_FIRST if self.p.mode == "sum" else BETA_NONE
+        for v in sorted(self.fwd_mat - {0}):
+            nd = self.nodes[v]
+            beta = beta_y if v == self.out else BETA_NONE
+            name = f"k{len(self.p.kernel_names)}_fwd_{nd.op}{v}"
+            tg = self.fwd_targets(v)
+            io = 4 * (nd.numel + self._input_numel(nd))
+            if nd.op == "fold":
+                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_fold(f, v, tg), 0, beta, f"fold {nd.attr['mode']} -> n{v}", io, 0)
+            elif nd.op == "softmax":
+                pre, span, post = self.softmax_geom(nd)
+                rows = math.prod(pre) * math.prod(post)
+                self.launch_pointwise(name, rows, lambda f, v=v, tg=tg: self.body_softmax(f, v, tg), 0, beta, f"softmax -> n{v}", io, 0)
+            elif nd.op == "fc":
+                self.lower_fc_fwd(name, v, tg, beta)
+            else:
+                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_map(f, v, tg), 0, beta, f"pointwise -> n{v}", io, 0)
+
+    def _input_numel(self, nd) -> int:
+        """Compulsory reads: materialised tensors the node's expression touches (once each)."""
+        seen, stack, tot = set(), list(nd.ins), 0
+        while stack:
+            v = stack.pop()
+            if v in seen:
+                continue
+            seen.add(v)
+            if v in self.fwd_mat:
+                tot += self.nodes[v].numel
+            else:
+                stack.extend(self.nodes[v].ins)
+        return tot
+
+    def coords_of(self, f: Fn, nd) -> tuple:
+        return tuple(f.decompose("r", nd.ext))
+
+    def body_map(self, f: Fn, v: int, targets) -> None:
+        nd = self.nodes[v]
+        f.computing = v
+        c = self.coords_of(f, nd)
+        x = self.compute(f, v, c)
+        for d, beta in targets:
+            f.store(d, c, x, beta)
+
+    def body_fold(self, f: Fn, v: int, targets) -> None:
+        nd = self.nodes[v]
+        dim, D, mode = nd.attr["dim"], nd.attr["D"], nd.attr["mode"]
+        c = self.coords_of(f, nd)
+        acc = f.fresh("acc")
+        if mode == "avg":
+            f.emit(f"float {acc} = 0.f;")
+        else:
+            cnt = f.fresh("cnt")
+            f.emit(f"float {acc} = -INFINITY; float {cnt} = 0.f;")
+        j = f.fresh("j")
+        f.open(f"for (int {j} = 0; {j} < {D}; ++{j})")
+        x = self.val(f, nd.ins[0], c[:dim] + (j,) + c[dim:])
+        if mode == "avg":
+            f.emit(f"{acc} += {x};")
+        else:
+            f.emit(f"if ({x} > {acc}) {{ {acc} = {x}; {cnt} = 1.f; }} else if ({x} == {acc}) {{ {cnt} += 1.f; }}")
+        f.close()
+        res = f.fvar(f"{acc} / {float(D)!r}f") if mode == "avg" else acc
+        for d, beta in targets:
+            f.store(d, c, res, beta)
+        if mode == "max":
+            f.store(self.count_desc[v], c, cnt, False)
+
+    def body_softmax(self, f: Fn, v: int, targets) -> None:
+        nd = self.nodes[v]
+        pre, span, post = self.softmax_geom(nd)
+        rc = f.decompose("r", pre + post)
+        pc, qc = tuple(rc[: len(pre)]), tuple(rc[len(pre) :])
+        S = math.prod(span)
+        mx, sm = f.fresh("mx"), f.fresh("sm")
+        f.emit(f"float {mx} = -INFINITY, {sm} = 0.f;")
+
+        def loop(stmt_fn):
+            j = f.fresh("j")
+            f.open(f"for (int {j} = 0; {j} < {S}; ++{j})")
+            sc = tuple(f.decompose(j, span))
+            c = pc + sc + qc
+            x = self.val(f, nd.ins[0], c)
+            stmt_fn(c, x)
+            f.close()
+
+        loop(lambda c, x: f.emit(f"{mx} = fmaxf({mx}, {x});"))
+        loop(lambda c, x: f.emit(f"{sm} += expf({x} - {mx});"))
+
+        def write(c, x):
+            y = f.fvar(f"expf({x} - {mx}) / {sm}")
+            for d, beta in targets:
+                f.store(d, c, y, beta)
+
+        loop(write)
+
+    # ---- FC
+    def fc_weight_slot(self, u: int) -> tuple[int, int]:
+        i = self.nodes[u].attr["fc_index"]
+        return self.p.slot_w(i), self.p.slot_dw(i)
+
+    def lower_fc_fwd(self, name, u, targets, beta) -> None:
+        nu = self.nodes[u]
+        v = nu.ins[0]
+        nv = self.nodes[v]
+        O, K = self.g.fc_shape(u)
+        S = math.prod(nu.sp_ext)
+        wslot, _ = self.fc_weight_slot(u)
+        io = 4 * (nu.numel + self._input_numel(nu))
+        flops = 2 * O * K * S
+        if min(O, K) <= SMALL_FC:
+
+            def body(f, u=u):
+                c = self.coords_of(f, nu)
+                o, sp = c[0], c[1:]
+                acc = f.fresh("acc")
+                f.emit(f"float {acc} = 0.f;")
+                wrow = f.ivar(f"{o}*{K}")
+                i = f.fresh("i")
+                f.open(f"for (int {i} = 0; {i} < {K}; ++{i})")
+                ch = tuple(f.decompose(i, nv.ch_ext))
+                x = self.val(f, v, ch + sp)
+                f.emit(f"{acc} = fmaf(__ldg({f.ptr(wslot)} + {wrow} + {i}), {x}, {acc});")
+                f.close()
+                for d, b in targets:
+                    f.store(d, c, acc, b)
+
+            self.launch_pointwise(name, nu.numel, body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops)
+            return
+        # A(m,k) = W[m*K + k];  B(n,k,s) = val(v)(decompose k | decompose s)
+        fa = Fn(self)
+        fa.pre = []
+        fa.computing = None
+        a_expr = f"__ldg({fa.ptr(wslot)} + m*{K} + k)"
+
+        def bfn(f):
+            ch = tuple(f.decompose("k", nv.ch_ext))
+            sp = tuple(f.decompose("s", nv.sp_ext))
+            return self.val(f, v, ch + sp)
+
+        def sfn(f, val):
+            c = ("m",) + tuple(f.decompose("s", nu.sp_ext))
+            for d, b in targets:
+                f.store(d, c, val, b)
+
+        self.emit_gemm_nk(name, fa, a_expr, bfn, sfn, M=O, K=K, S=S, phase=0, beta=beta, what=f"fc {O}x{K}x{S} -> n{u}", nbytes=io, flops=flops)
+
+    def emit_gemm_nk(self, name, fa: Fn, a_expr: str, bfn, sfn, M, K, S, phase, beta, what, nbytes, flops) -> None:
+        """C[n][m][s] = sum_k A(m,k) * B(n,k,s) through canvas::gemm_nk (one shared slot table)."""
+        fb = Fn(self)
+        fb.pre = []
+        fb.computing = None
+        fb.local_slots = fa.local_slots  # share the pointer table
+        bval = bfn(fb)
+        fs = Fn(self)
+        fs.pre = []
+        fs.computing = None
+        fs.local_slots = fa.local_slots
+        sfn(fs, "acc")
+        lines = [
+            f"struct {name}_F {{",
+            f"  static constexpr int M = {M}, K = {K}, S = {S};",
+            "  static __device__ __forceinline__ float A(const CanvasArgs& a, const int m, const int k) {",
+            f"    return {a_expr};",
+            "  }",
+            "  static __device__ __forceinline__ float B(const CanvasArgs& a, const long long n, const int k, const int s) {",
+        ]
+        lines += ["    " + s for s in fb.pre] + fb.lines + [f"    return {bval};", "  }"]
+        lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
+        lines += ["    " + s for s in fs.pre] + fs.lines + ["  }", "};"]
+        functor = "\n".join(lines) + "\n"
+        launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_nk<{name}_F>(a); }}\n'
+        k = self.add_kernel(name, functor, launcher)
+        grid = (GridRule(S, 0, GEMM_TILE), GridRule(0, M, GEMM_TILE), GridRule(0, 1, 1))
+        self.p.launches.append(Launch("kernel", phase, name, k, 256, grid, tuple(fa.local_slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+
+    def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops) -> None:
+        """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
+        tchunk = max(2048, -(-4096 * S // 60000) * GEMM_TILE)
+        k_ws, pdesc = self._new_ws((1,))
+        self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
+        fa, fb = Fn(self), Fn(self)
+        fa.pre, fb.pre = [], []
+        fa.computing = fb.computing = None
+        fb.local_slots = fa.local_slots
+        aval = afn(fa)
+        bval = bfn(fb)
+        pslot_local = fa.ptr(-1 - k_ws)  # partials (fixed up to the real ws slot in finish())
+        lines = [
+            f"struct {name}_F {{",
+            f"  static constexpr int M = {M}, J = {J}, S = {S}, TCHUNK = {tchunk};",
+            "  static __device__ __forceinline__ float A(const CanvasArgs& a, const long long n, const int m, const int s) {",
+        ]
+        lines += ["    " + s for s in fa.pre] + fa.lines + [f"    return {aval};", "  }"]
+        lines += ["  static __device__ __forceinline__ float B(const CanvasArgs& a, const long long n, const int k, const int s) {"]
+        lines += ["    " + s for s in fb.pre] + fb.lines + [f"    return {bval};", "  }"]
+        lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
+        lines += ["};"]
+        functor = "\n".join(lines) + "\n"
+        launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_wgrad<{name}_F>(a); }}\n'
+        k = self.add_kernel(name, functor, launcher)
+        grid = (GridRule(0, J, GEMM_TILE), GridRule(0, M, GEMM_TILE), GridRule(S, 0, tchunk))
+        self.p.launches.append(Launch("kernel", 1, name, k, 256, grid, tuple(fa.local_slots), BETA_NONE, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+        # ordered reduction of the partials into dW
+        rname = name + "_reduce"
+        rsrc = (
+            f"struct {rname}_F {{ static constexpr int MJ = {M * J}, S = {S}, TCHUNK = {tchunk}; }};\n"
+            f'extern "C" __global__ void __launch_bounds__(256) {rname}(const CanvasArgs a) {{ canvas::reduce_partials<{rname}_F>(a); }}\n'
+        )
+        k2 = self.add_kernel(rname, "", rsrc)
+        grid2 = (GridRule(0, M * J, 256), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        self.p.launches.append(Launch("kernel", 1, rname, k2, 256, grid2, (-1 - k_ws, dw_slot), BETA_NONE, what=f"wgrad reduce {M}x{J}"))
+
+    # ---- backward
+    def lower_backward(self) -> None:
+        p = self.p
+        self.dy_desc = self.y_desc(SLOT_DY)
+        stride_gt1 = p.stride > 1
+        dx_beta = BETA_ALWAYS if stride_gt1 else (BETA_AFTER_FIRST if (p.copies > 1 and p.mode == "concat") else BETA_NONE)
+        if stride_gt1:
+            p.launches.append(Launch("memset", 1, "dx_zero", memset_slot=SLOT_DX, memset_size=SizeRule(4 * p.c_in * p.h_in * p.w_in, 1, 0), what="dx zero-fill (stride > 1)"))
+        # where each materialised gradient lives
+        for v in sorted(self.grad_mat):
+            nd = self.nodes[v]
+            if v == 0:
+                self.grad_desc[0] = self.dx_desc()
+                continue
+            only_fc = len(nd.consumers) == 1 and self.nodes[nd.consumers[0][0]].op == "fc"
+            if only_fc:
+                continue  # the FC dgrad writes this gradient directly (no extra pass)
+            _, d = self._new_ws(nd.ext)
+            self.grad_desc[v] = d
+        for u in sorted(self.nodes[i].id for i in range(len(self.nodes)) if self.nodes[i].op == "fc"):
+            v = self.nodes[u].ins[0]
+            nv = self.nodes[v]
+            if v in self.grad_mat and len(nv.consumers) == 1:
+                if v == 0:
+                    self.dgrad_desc[u] = self.dx_desc()
+                else:
+                    _, d = self._new_ws(nv.ext)
+                    self.dgrad_desc[u] = d
+                    self.grad_desc[v] = d
+            else:
+                _, d = self._new_ws(nv.ext)
+                self.dgrad_desc[u] = d
+        for u in (nd.id for nd in self.nodes if nd.op == "softmax"):
+            pre, span, post = self.softmax_geom(self.nodes[u])
+            _, self.dot_desc[u] = self._new_ws(pre + post)
+
+        for u in range(len(self.nodes) - 1, -1, -1):
+            nu = self.nodes[u]
+            # 1) materialise dL/du if it is a gradient sum point (not dy, not aliased to an FC dgrad)
+            if u in self.grad_mat and not self._grad_is_fc_alias(u):
+                beta = dx_beta if u == 0 else BETA_NONE
+                d = self.grad_desc[u]
+                name = f"k{len(p.kernel_names)}_bwd_grad{u}"
+                self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0)
+            # 2) adjoint kernels of the producer edge that need dL/du as a whole
+            if nu.op == "fc":
+                self.lower_fc_bwd(u, dx_beta)
+            elif nu.op == "softmax":
+                self.lower_softmax_dot(u)
+
+    def _grad_is_fc_alias(self, v: int) -> bool:
+        nd = self.nodes[v]
+        return len(nd.consumers) == 1 and self.nodes[nd.consumers[0][0]].op == "fc"
+
+    def body_grad(self, f: Fn, v: int, d: TDesc) -> None:
+        nd = self.nodes[v]
+        c = self.coords_of(f, nd)
+        self.computing_grad = v
+        g = self.grad_sum(f, v, c)
+        self.computing_grad = None
+        f.store(d, c, g, v == 0)
+
+    def lower_softmax_dot(self, u: int) -> None:
+        nu = self.nodes[u]
+        pre, span, post = self.softmax_geom(nu)
+        rows = math.prod(pre) * math.prod(post)
+        S = math.prod(span)
+        d = self.dot_desc[u]
+
+        def body(f):
+            rc = f.decompose("r", pre + post)
+            pc, qc = tuple(rc[: len(pre)]), tuple(rc[len(pre) :])
+            acc = f.fresh("acc")
+            f.emit(f"float {acc} = 0.f;")
+            j = f.fresh("j")
+            f.open(f"for (int {j} = 0; {j} < {S}; ++{j})")
+            c = pc + tuple(f.decompose(j, span)) + qc
+            g = self.grad(f, u, c)
+            y = self.val(f, u, c)
+            f.emit(f"{acc} = fmaf({g}, {y}, {acc});")
+            f.close()
+            f.store(d, pc + qc, acc, False)
+
+        name = f"k{len(self.p.kernel_names)}_bwd_softmaxdot{u}"
+        self.launch_pointwise(name, rows, body, 1, BETA_NONE, f"softmax row-dot n{u}", 4 * (2 * nu.numel + rows), 0)
+
+    def lower_fc_bwd(self, u: int, dx_beta: int) -> None:
+        nu = self.nodes[u]
+        v = nu.ins[0]
+        nv = self.nodes[v]
+        O, K = self.g.fc_shape(u)
+        S = math.prod(nu.sp_ext)
+        wslot, dwslot = self.fc_weight_slot(u)
+        dd = self.dgrad_desc[u]
+        beta = dx_beta if dd.slot == SLOT_DX else BETA_NONE
+        flops = 2 * O * K * S
+        # dgrad: D[n,i,s] = sum_o W[o,i] * dL/du[n,o,s]
+        name = f"k{len(self.p.kernel_names)}_bwd_dgrad{u}"
+        if min(O, K) <= SMALL_FC:
+
+            def body(f):
+                c = self.coords_of(f, nv)
+                i = f.flatten(c[: nv.nch], nv.ch_ext)
+                sp = c[nv.nch :]
+                acc = f.fresh("acc")
+                f.emit(f"float {acc} = 0.f;")
+                o = f.fresh("o")
+                f.open(f"for (int {o} = 0; {o} < {O}; ++{o})")
+                g = self.grad(f, u, (o,) + sp)
+                f.emit(f"{acc} = fmaf(__ldg({f.ptr(wslot)} + {o}*{K} + {i}), {g}, {acc});")
+                f.close()
+                f.store(dd, c, acc, beta != BETA_NONE)
+
+            self.launch_pointwise(name, nv.numel, body, 1, beta, f"dgrad_small {O}x{K} n{u}->n{v}", 4 * (nu.numel + nv.numel), flops)
+        else:
+            fa = Fn(self)
+            fa.pre = []
+            fa.computing = None
+            a_expr = f"__ldg({fa.ptr(wslot)} + k*{K} + m)"
+
+            def bfn(f):
+                sp = tuple(f.decompose("s", nu.sp_ext))
+                return self.grad(f, u, ("k",) + sp)
+
+            def sfn(f, val):
+                c = tuple(f.decompose("m", nv.ch_ext)) + tuple(f.decompose("s", nv.sp_ext))
+                f.store(dd, c, val, beta != BETA_NONE)
+
+            self.emit_gemm_nk(name, fa, a_expr, bfn, sfn, M=K, K=O, S=S, phase=1, beta=beta, what=f"dgrad {K}x{O}x{S} n{u}->n{v}", nbytes=4 * (nu.numel + nv.numel), flops=flops)
+        # wgrad: dW[o,i] = sum_{n,s} dL/du[n,o,s] * v[n,i,s]
+        name = f"k{len(self.p.kernel_names)}_bwd_wgrad{u}"
+
+        def afn(f):
+            sp = tuple(f.decompose("s", nu.sp_ext))
+            return self.grad(f, u, ("m",) + sp)
+
+        def bfn2(f):
+            ch = tuple(f.decompose("k", nv.ch_ext))
+            sp = tuple(f.decompose("s", nv.sp_ext))
+            return self.val(f, v, ch + sp)
+
+        self.emit_gemm_wgrad(name, afn, bfn2, O, K, S, dwslot, f"wgrad {O}x{K} over {S}/img n{u}", 4 * (nu.numel + self._input_numel(nu)), flops)
+
+    # -------------------------------------------------------------- assemble
+    def finish(self) -> None:
+        p = self.p
+        nsv = len(p.saved)
+        fix = lambda s: p.slot_ws(-1 - s) if s < 0 else s  # noqa: E731
+        for L in p.launches:
+            L.slots = tuple(fix(s) for s in L.slots)
+        header = '#include "canvas_kernels.cuh"\n'
+        p.source = header + "\n".join(self.kernels)
+        del nsv
+
+
+def lower(g: ConcreteGraph, *, c_in: int, c_out: int, stride: int = 1, h_in: int | None = None, w_in: int | None = None) -> Plan:
+    """Build the fwd+bwd plan of one replacement target (SPEC.md:417-425 Fig.-2, App. A.10).
+
+    ``g`` is evaluated at C = min(c_in, c_out) and the *output* resolution;
+    ``h_in``/``w_in`` are the full-resolution input extents (stride policy:
+    x[..., ::s, ::s] first, fused into the first loads).
+    """
+    c = g.nodes[0].ext[0]
+    if c != min(c_in, c_out) or max(c_in, c_out) % c:
+        raise LoweringError(f"C={c} does not replicate to {c_in}->{c_out}")
+    h, w = g.nodes[0].ext[1:]
+    h_in = h_in if h_in is not None else h * stride
+    w_in = w_in if w_in is not None else w * stride
+    if -(-h_in // stride) != h or -(-w_in // stride) != w:
+        raise LoweringError(f"stride {stride} maps {h_in}x{w_in} to {-(-h_in // stride)}x{-(-w_in // stride)}, kernel is {h}x{w}")
+    r = max(c_in, c_out) // c
+    mode = "concat" if c_out >= c_in else "sum"
+    p = Plan(g, c_in, c_out, stride, h_in, w_in, r, mode)
+    hw_in, hw = h_in * w_in, h * w
+    if mode == "concat":
+        p.y_copy_off = c * hw
+        p.dy_copy_off = c * hw
+    else:
+        p.x_copy_off = c * hw_in
+        p.dx_copy_off = c * hw_in
+    lw = Lowerer(g, p)
+    lw.lower_forward()
+    lw.lower_backward()
+    lw.finish()
+    p.fwd_mat = lw.fwd_desc
+    return p
+
+
+# ------------------------------------------------------------------ derivatives
+def _bc_d_rhs(op: str, g: str, l: str, r: str) -> str:
+    if op == "add":
+        return g
+    if op == "sub":
+        return f"-{g}"
+    if op == "mul":
+        return f"{g} * {l}"
+    if op == "min":
+        return f"({r} < {l} ? {g} : ({r} == {l} ? 0.5f * {g} : 0.f))"
+    if op == "max":
+        return f"({r} > {l} ? {g} : ({r} == {l} ? 0.5f * {g} : 0.f))"
+    raise LoweringError(op)
+
+
+def _bc_d_lhs(op: str, g: str, l: str, r: str) -> str:
+    if op in ("add", "sub"):
+        return g
+    if op == "mul":
+        return f"{g} * {r}"
+    if op == "min":
+        return f"({l} < {r} ? {g} : ({l} == {r} ? 0.5f * {g} : 0.f))"
+    if op == "max":
+        return f"({l} > {r} ? {g} : ({l} == {r} ? 0.5f * {g} : 0.f))"
+    raise LoweringError(op)

@@ -1,0 +1,90 @@
+// TEST INFRASTRUCTURE ONLY: host (g++) emulation of csrc/kernels/canvas_kernels.cuh.
+//
+// The lowering emits CUDA functors; compiling them against this header on
+// the CPU lets the CPU test-suite check the *generated* index maps, adjoint
+// gathers and launch schedule against the oracle without a GPU.  The
+// templates here are plain sequential loops with the same reduction order as
+// the device templates where it matters (wgrad partial chunks); the device
+// tiling itself is checked by the GPU parity tests.
+#pragma once
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#define __device__
+#define __global__
+#define __forceinline__ inline
+#define __launch_bounds__(x)
+#define __restrict__
+using std::max;
+using std::min;
+template <class T>
+inline T __ldg(const T* p) { return *p; }
+
+#define CANVAS_MAX_KSLOTS 24
+struct CanvasArgs {
+  float* p[CANVAS_MAX_KSLOTS];
+  long long n;
+  int beta;
+  int copy;
+};
+
+namespace canvas {
+template <class F>
+void pointwise(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int r = 0; r < (int)F::PER; ++r) F::run(a, n, r);
+}
+
+template <class F>
+void gemm_nk(const CanvasArgs& a) {
+  const long long T = a.n * (long long)F::S;
+  float* col = new float[F::K];
+  for (long long t = 0; t < T; ++t) {
+    const long long n = t / F::S;
+    const int s = (int)(t - n * F::S);
+    for (int k = 0; k < F::K; ++k) col[k] = F::B(a, n, k, s);
+    for (int m = 0; m < F::M; ++m) {
+      float acc = 0.f;
+      for (int k = 0; k < F::K; ++k) acc = std::fma(F::A(a, m, k), col[k], acc);
+      F::store(a, n, m, s, acc);
+    }
+  }
+  delete[] col;
+}
+
+template <class F>
+void gemm_wgrad(const CanvasArgs& a) {
+  const long long T = a.n * (long long)F::S;
+  const long long Z = (T + F::TCHUNK - 1) / F::TCHUNK;
+  float* av = new float[F::M];
+  float* bv = new float[F::J];
+  for (long long z = 0; z < Z; ++z) {
+    float* P = F::partials(a) + z * F::M * F::J;
+    std::memset(P, 0, sizeof(float) * F::M * F::J);
+    const long long te = std::min<long long>((z + 1) * F::TCHUNK, T);
+    for (long long t = z * F::TCHUNK; t < te; ++t) {
+      const long long n = t / F::S;
+      const int s = (int)(t - n * F::S);
+      for (int m = 0; m < F::M; ++m) av[m] = F::A(a, n, m, s);
+      for (int j = 0; j < F::J; ++j) bv[j] = F::B(a, n, j, s);
+      for (int m = 0; m < F::M; ++m)
+        for (int j = 0; j < F::J; ++j) P[m * F::J + j] = std::fma(av[m], bv[j], P[m * F::J + j]);
+    }
+  }
+  delete[] av;
+  delete[] bv;
+}
+
+template <class F>
+void reduce_partials(const CanvasArgs& a) {
+  const long long T = a.n * (long long)F::S;
+  const int Z = (int)((T + F::TCHUNK - 1) / F::TCHUNK);
+  for (int idx = 0; idx < F::MJ; ++idx) {
+    float s = 0.f;
+    for (int z = 0; z < Z; ++z) s += a.p[0][(long long)z * F::MJ + idx];
+    a.p[1][idx] = s;
+  }
+}
+}  // namespace canvas

@@ -1,0 +1,97 @@
+"""GPU parity: the sm_100a executor (through the C ABI) vs the fp64 CPU oracle.
+
+Covers every pinned kernel, Fig.-2 replication in both
+directions with the stride-2 policy, the first 20 kernels of the reference
+sampler (nodes=10, seed=7), the im2col calibration against cuDNN-free
+F.conv2d semantics, determinism, and the CanvasConv2d module path.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2304_07741_b200 import zoo
+from parity import assert_close, reference
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(case):
+    from paper_2304_07741_b200.executor import device_plan
+
+    dev = torch.device("cuda:0")
+    dp = device_plan(case.plan, 0)
+    x = case.x.float().to(dev)
+    ws = [w.float().to(dev).contiguous() for c in case.weights for w in c]
+    n = x.shape[0]
+    saved_b, ws_b = dp.sizes(n)
+    y = torch.full(tuple(case.y.shape), float("nan"), device=dev)
+    saved = torch.empty(max(saved_b, 1), dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    dp.forward(x, ws, y, saved, st)
+    dy = case.dy.float().to(dev)
+    dx = torch.full_like(x, float("nan")) if case.plan.stride == 1 else torch.full_like(x, 7.0)
+    dws = [torch.full_like(w, float("nan")) for w in ws]
+    work = torch.empty(max(ws_b, 1), dtype=torch.uint8, device=dev)
+    dp.backward(x, ws, saved, dy, dx, dws, work, st)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), dx.cpu().numpy(), [d.cpu().numpy() for d in dws]
+
+
+@pytest.mark.parametrize("name", list(zoo.ALL))
+def test_pinned_config1(name):
+    """Config-1 shapes (C=64, 56x56), batch 2."""
+    case = reference(zoo.ALL[name], 64, 64, 56, 56, n=2)
+    y, dx, dws = run_gpu(case)
+    assert_close(case, y, dx, dws, name)
+
+
+@pytest.mark.parametrize("cin,cout,stride", [(16, 32, 2), (32, 16, 1), (16, 64, 2), (16, 16, 2)])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution", "seed7_k0"])
+def test_replication_and_stride(name, cin, cout, stride):
+    case = reference(zoo.ALL[name], cin, cout, 14, 13, stride=stride, n=3)
+    y, dx, dws = run_gpu(case)
+    assert_close(case, y, dx, dws, f"{name} {cin}->{cout} s{stride}")
+
+
+def _sweep(path):
+    text = open(path).read()
+    return ["canvas-ir v1\n" + t for t in text.split("canvas-ir v1\n")[1:]]
+
+
+@pytest.mark.parametrize("i", range(20))
+def test_sampler_sweep_first20(i):
+    texts = _sweep("tests/golden/sampler_10_7_20.cir")
+    case = reference(texts[i], 32, 32, 12, 12, n=2)
+    y, dx, dws = run_gpu(case)
+    assert_close(case, y, dx, dws, f"sweep #{i}")
+
+
+def test_deterministic():
+    case = reference(zoo.SEED7_K1, 64, 64, 28, 28, n=4)
+    a = run_gpu(case)
+    b = run_gpu(case)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert all(np.array_equal(u, v) for u, v in zip(a[2], b[2]))
+
+
+def test_im2col_is_conv():
+    """SPEC.md:509 derived oracle: unfold(h); unfold(w); fc(C) == conv2d(padding=1)."""
+    case = reference(zoo.IM2COL, 64, 64, 20, 20, n=2)
+    y, _, _ = run_gpu(case)
+    w = case.weights[0][0].view(64, 64, 3, 3)
+    ref = torch.nn.functional.conv2d(case.x, w, padding=1).numpy()
+    assert np.max(np.abs(y - ref)) <= 1e-5 + 1e-4 * np.max(np.abs(ref))
+
+
+def test_module_autograd():
+    from paper_2304_07741_b200.module import CanvasConv2d
+
+    torch.manual_seed(0)
+    m = CanvasConv2d(zoo.SEED7_K1, 32, 64, 3, stride=2).cuda()
+    x = torch.randn(3, 32, 16, 16, device="cuda", requires_grad=True)
+    y = m(x)
+    assert y.shape == (3, 64, 8, 8)
+    y.square().sum().backward()
+    assert x.grad is not None and torch.isfinite(x.grad).all()
+    assert all(p.grad is not None and torch.isfinite(p.grad).all() for p in m.weights)
