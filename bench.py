@@ -1,0 +1,406 @@
+"""Canvas-ResNet-18 training throughput on B200 (BASELINE.json metric, config 2).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--kernel seed7_k1] [--batch 256]
+
+Workload (config 2): torchvision ResNet-18 with all 16 3x3 convs
+replaced by one sampled Canvas kernel (default: seed-7 kernel #1, the
+Unfold+FC tensor case; G=4, K=3, stride-2 targets subsample first, Fig.-2
+r-copy concat), synthetic ImageNet 224^2, per-GPU batch 256 (weak scaling),
+fp32, CE loss + SGD(momentum) step.  One step = one fwd+bwd+update of one
+batch per GPU.  N>1: one process per GPU (torchrun), DDP gradient allreduce
+over NCCL — the only collective.
+
+Timing: W warm-up steps, barrier + synchronize, CUDA events around K steps
+on the compute stream, synchronize + barrier, max over ranks.  Inputs are
+larger than L2 (154 MB of images per step + >1 GB of activations), so no
+explicit flush.  ``e2e`` repeats the step with the batch copied from pinned
+host memory and the loss read back every step.  ``roofline`` times the
+dominant Canvas kernel (the K=9C FC GEMM of the layer1 targets) with CUDA
+events recorded by libcanvas around each of its launches during the timed
+region.  ``cpu_baseline`` / ``--impl reference`` time the CPU restatement
+(oracle/torch_ref.py, torch fp32 on all host cores) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+import torch.nn.functional as F  # noqa: E402
+
+from paper_2304_07741_b200 import zoo  # noqa: E402
+
+METRIC = "images/sec fwd+bwd (Canvas-ResNet-18, 224²) at 1/2/4/8 B200; % roofline/kernel"
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+
+
+def build_model(kernel: str, device=None, cpu_reference: bool = False):
+    import torchvision
+
+    from paper_2304_07741_b200.module import replace
+
+    torch.manual_seed(0)
+    m = torchvision.models.resnet18(num_classes=1000)
+    text = zoo.ALL[kernel]
+    if cpu_reference:
+        from oracle.torch_ref import CanvasConvRef
+
+        def factory(conv):
+            return CanvasConvRef(text, conv.in_channels, conv.out_channels, 8, 8, 3, 3, stride=conv.stride[0], g=4, seed=None)
+
+        names = replace(m, text, factory=factory)
+    else:
+        names = replace(m, text, g=4)
+    assert len(names) == 16, names
+    return m.to(device) if device is not None else m
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = "index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        rows = [r.split(", ") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+class CpuReference:
+    """CPU restatement (oracle/torch_ref.py, torch fp32, all host threads) of Canvas-ResNet-18."""
+
+    def __init__(self, kernel: str, batch: int = 2):
+        torch.set_num_threads(os.cpu_count() or 1)
+        self.kernel, self.batch = kernel, batch
+        self.m = build_model(kernel, cpu_reference=True)
+        self.opt = torch.optim.SGD(self.m.parameters(), lr=0.01, momentum=0.9)
+        g = torch.Generator().manual_seed(0)
+        self.x = torch.randn(batch, 3, 224, 224, generator=g)
+        self.y = torch.randint(0, 1000, (batch,), generator=g)
+
+    def step(self) -> None:
+        self.opt.zero_grad(set_to_none=True)
+        F.cross_entropy(self.m(self.x), self.y).backward()
+        self.opt.step()
+
+    def timed(self, budget_s: float) -> dict:
+        n, t0 = 0, time.perf_counter()
+        while True:
+            self.step()
+            n += 1
+            if time.perf_counter() - t0 >= budget_s:
+                break
+        dt = time.perf_counter() - t0
+        return {"value": n * self.batch / dt, "unit": "images/s", "cores": torch.get_num_threads(), "steps": n, "seconds": round(dt, 2), "sample": f"{n} fwd+bwd+SGD steps of batch {self.batch} at 224^2 through Canvas-ResNet-18 ({self.kernel}) in torch fp32 on CPU ({self.cores_desc()})"}
+
+    @staticmethod
+    def cores_desc() -> str:
+        model = ""
+        try:
+            with open("/proc/cpuinfo") as f:
+                model = next((ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name")), "")
+        except OSError:
+            pass
+        return f"{os.cpu_count()} threads, {model}"
+
+
+def cpu_sample(kernel: str, budget_s: float, batch: int = 2) -> dict:
+    ref = CpuReference(kernel, batch)
+    ref.step()  # warm-up
+    return ref.timed(budget_s)
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """Reference arm: the CPU restatement of the path on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    ref = CpuReference(args.kernel)
+    for _ in range(args.warmup):
+        ref.step()
+    per_step = []
+    r = None
+    for _ in range(args.steps):
+        r = ref.timed(args.ref_seconds / max(1, args.steps))
+        per_step.append(r["value"])
+    val = statistics.mean(per_step)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": round(val, 3),
+        "unit": "images/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(1000.0 * ref.batch / val, 1),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"Canvas-ResNet-18 ({args.kernel}) fwd+bwd+SGD, 224^2, CPU restatement, batch {ref.batch} per timed sample", "kernel": args.kernel},
+        "cpu_baseline": {"value": round(val, 3), "unit": "images/s", "cores": r["cores"], "kind": "port", "sample": r["sample"]},
+        "e2e": {"value": round(val, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--kernel", default="seed7_k1", choices=sorted(zoo.ALL))
+    ap.add_argument("--impl", default="canvas", choices=["canvas", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=30.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-context", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "canvas" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.benchmark = True
+
+    model = build_model(args.kernel, dev)
+    if world > 1:
+        from torch.nn.parallel import DistributedDataParallel as DDP
+
+        model = DDP(model, device_ids=[local], bucket_cap_mb=25, gradient_as_bucket_view=True)
+    opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn(args.batch, 3, 224, 224, device=dev, generator=gen)
+    lab = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+
+    def step(xb, yb):
+        opt.zero_grad(set_to_none=True)
+        loss = F.cross_entropy(model(xb), yb)
+        loss.backward()
+        opt.step()
+        return loss
+
+    t_build = time.perf_counter()
+    for _ in range(args.warmup):
+        step(x, lab)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t_build
+
+    # --- dominant-kernel events (layer1 target: 64->64 at 56x56, FC K = 9C GEMM) ---
+    from paper_2304_07741_b200.module import CanvasConv2d
+
+    core = model.module if world > 1 else model
+    l1 = core.layer1[0].conv1
+    assert isinstance(l1, CanvasConv2d)
+    dp = l1.device_plan(x.new_empty(1, 64, 56, 56))
+    fc_nodes = dp.plan.graph.fc_nodes
+    big = max(fc_nodes, key=lambda v: dp.plan.graph.fc_shape(v)[1])
+    rec = next(i for i, L in enumerate(dp.plan.launches) if L.kind == "kernel" and L.phase == 0 and L.name.endswith(f"fc{big}"))
+    L = dp.plan.launches[rec]
+    launches_per_step = 4 * 2  # layer1: 4 convs share this plan; +fwd of each (x1) -> 4 launches; keep 2x margin
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(launches_per_step * args.steps)]
+    for a, b in evs:
+        a.record()
+        b.record()
+    dp.profile(rec, evs)
+
+    per_step_launches = 0
+    for m in core.modules():
+        if isinstance(m, CanvasConv2d):
+            for p in m._plans.values():
+                per_step_launches += p.launches(0) + p.launches(1)
+
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step(x, lab)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    nprof = dp.profile_count()
+    dp.profile(rec, [])
+    k_times = [a.elapsed_time(b) for a, b in evs[: min(nprof, len(evs))]]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * args.batch * 1000.0 / ms
+
+    # --- e2e: batch from pinned host memory each step, loss read back each step ---
+    xh = x.cpu().pin_memory()
+    lh = lab.cpu().pin_memory()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record()
+    e2e_steps = max(2, args.steps // 2)
+    for _ in range(e2e_steps):
+        xb = xh.to(dev, non_blocking=True)
+        yb = lh.to(dev, non_blocking=True)
+        loss = step(xb, yb)
+        float(loss.item())
+    e3.record()
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3) / e2e_steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    del t0
+    e2e = world * args.batch * 1000.0 / ms_e2e
+
+    # --- roofline of the dominant kernel ---
+    pk = peaks()
+    o, kdim = dp.plan.graph.fc_shape(big)
+    s = 56 * 56
+    flops = 2.0 * o * kdim * s * args.batch
+    avg_ms = statistics.mean(k_times) if k_times else float("nan")
+    achieved = flops / (avg_ms * 1e-3) / 1e12
+    tf32_peak = pk["bf16_tflops"] / 2.0
+    roofline = {
+        "bound": "tensor",
+        "kernel": L.name,
+        "achieved": round(achieved, 2),
+        "peak": round(tf32_peak, 1),
+        "unit": "TFLOP/s",
+        "frac": round(achieved / tf32_peak, 4),
+        "traffic": None,
+        "launch_ms": round(avg_ms, 4),
+        "launches_timed": len(k_times),
+        "algorithmic": f"2*{o}*{kdim}*{s}*{args.batch} FLOP per launch (SURVEY §8d: 2 x FC MACs)",
+        "peak_source": "TF32 dense = 1/2 of MEASURED_PEAKS.json bf16_tflops (burst); fp32 SIMT path this round",
+    }
+    prof_json = os.path.join(ROOT, "profiles", "dominant_traffic.json")
+    if os.path.exists(prof_json):
+        try:
+            with open(prof_json) as f:
+                tr = json.load(f).get(args.kernel)
+            if tr and tr.get("batch") == args.batch:
+                roofline["traffic"] = tr["dram_bytes"]
+        except (OSError, ValueError):
+            pass
+
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "images/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": "config 2: torchvision ResNet-18, all 16 3x3 convs -> one Canvas kernel, fwd+bwd+SGD",
+            "kernel": args.kernel,
+            "global_batch": args.batch * world,
+            "per_gpu_batch": args.batch,
+            "image": "3x224x224 synthetic N(0,1), random-init weights",
+            "parallelism": f"dp{world}",
+            "G": 4,
+            "K": 3,
+            "l2": "inputs larger than L2 (no flush)",
+        },
+        "e2e": {"value": round(e2e, 2), "unit": "images/s", "h2d_bytes_per_step": int(xh.numel() * 4 + lh.numel() * 8), "d2h_bytes_per_step": 4},
+        "gpu_launches": per_step_launches * args.steps,
+        "roofline": roofline,
+        "clocks": clk,
+        "warmup_s": round(t_build, 1),
+    }
+    if rank == 0 and world == 1 and not args.no_context:
+        line["context"] = context_numbers(args, dev)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = {k: v for k, v in cpu_sample(args.kernel, args.cpu_seconds).items() if k in ("value", "unit", "cores", "sample")}
+        line["cpu_baseline"]["kind"] = "port"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def context_numbers(args, dev) -> dict:
+    """Unreplaced torchvision ResNet-18 (cuDNN, fp32 with TF32 off) for context only."""
+    import torchvision
+
+    torch.manual_seed(0)
+    m = torchvision.models.resnet18(num_classes=1000).to(dev)
+    opt = torch.optim.SGD(m.parameters(), lr=0.01, momentum=0.9)
+    x = torch.randn(args.batch, 3, 224, 224, device=dev)
+    y = torch.randint(0, 1000, (args.batch,), device=dev)
+
+    def step():
+        opt.zero_grad(set_to_none=True)
+        F.cross_entropy(m(x), y).backward()
+        opt.step()
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(5):
+        step()
+    b.record()
+    torch.cuda.synchronize()
+    return {"resnet18_cudnn_fp32_images_s": round(args.batch * 5 * 1000.0 / a.elapsed_time(b), 1)}
+
+
+if __name__ == "__main__":
+    main()

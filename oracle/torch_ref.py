@@ -238,22 +238,45 @@ def conv_replacement(ck: Concrete, x: torch.Tensor, weights: list[list[torch.Ten
 
 
 class CanvasConvRef(torch.nn.Module):
-    """CPU torch module computing a Canvas conv replacement (reference path)."""
+    """CPU torch module computing a Canvas conv replacement (reference path).
 
-    def __init__(self, ir_text: str, c_in: int, c_out: int, h: int, w: int, kh: int, kw: int, stride: int = 1, g: int = 4, xs: dict | None = None, seed: int = 2):
+    The concrete graph depends on the input resolution (H, W are constants of
+    the assignment), so it is rebuilt lazily per input size; the FC weight
+    shapes only depend on channel dims and are fixed at construction.
+    """
+
+    def __init__(self, ir_text: str, c_in: int, c_out: int, h: int, w: int, kh: int, kw: int, stride: int = 1, g: int = 4, xs: dict | None = None, seed: int | None = 2):
         super().__init__()
-        c = min(c_in, c_out)
-        t = cir.parse(ir_text).template
-        consts = {"C": c, "G": g, "H": -(-h // stride), "W": -(-w // stride), "KH": kh, "KW": kw}
-        a = Assignment(consts, dict(xs if xs is not None else proportional_values(t, consts)))
-        self.ck = concretize(t, a)
+        self.text, self.g, self.kh, self.kw, self.xs = ir_text, g, kh, kw, xs
         self.c_in, self.c_out, self.stride = c_in, c_out, stride
-        r = max(c_in, c_out) // c
-        ws = init_weights(self.ck, copies=r, seed=seed)
+        c = min(c_in, c_out)
+        self.r = max(c_in, c_out) // c
+        ck = self._concrete(max(h, 8 * stride), max(w, 8 * stride))
+        if seed is None:
+            ws = []
+            for _ in range(self.r):
+                cw = []
+                for o, k in fc_weight_shapes(ck):
+                    b = 1.0 / math.sqrt(k)
+                    cw.append(torch.empty(o, k).uniform_(-b, b))
+                ws.append(cw)
+        else:
+            ws = init_weights(ck, copies=self.r, seed=seed)
         self.weights = torch.nn.ParameterList([torch.nn.Parameter(w) for copy in ws for w in copy])
-        self.r = r
-        self.nfc = len(self.ck.fc_edges)
+        self.nfc = len(ck.fc_edges)
+        self._cks: dict = {}
+
+    def _concrete(self, h: int, w: int) -> Concrete:
+        c = min(self.c_in, self.c_out)
+        t = cir.parse(self.text).template
+        consts = {"C": c, "G": self.g, "H": -(-h // self.stride), "W": -(-w // self.stride), "KH": self.kh, "KW": self.kw}
+        a = Assignment(consts, dict(self.xs if self.xs is not None else proportional_values(t, consts)))
+        return concretize(t, a)
 
     def forward(self, x):
+        key = tuple(x.shape[2:])
+        ck = self._cks.get(key)
+        if ck is None:
+            ck = self._cks[key] = self._concrete(*key)
         ws = [list(self.weights[j * self.nfc : (j + 1) * self.nfc]) for j in range(self.r)]
-        return conv_replacement(self.ck, x, ws, self.c_in, self.c_out, self.stride)
+        return conv_replacement(ck, x, ws, self.c_in, self.c_out, self.stride)

@@ -61,6 +61,7 @@ struct Driver {
   CUresult (*cuMemsetD8Async)(CUdeviceptr, unsigned char, size_t, CUstream);
   CUresult (*cuGetErrorString)(CUresult, const char**);
   CUresult (*cuFuncSetAttribute)(CUfunction, int, int);
+  CUresult (*cuEventRecord)(void*, CUstream);
 };
 
 // ----------------------------------------------------------------- NVRTC
@@ -110,7 +111,7 @@ Driver& driver() {
            sym(h, "cuModuleGetFunction", d.cuModuleGetFunction, w) &&
            sym(h, "cuLaunchKernel", d.cuLaunchKernel, w) && sym(h, "cuMemsetD8Async", d.cuMemsetD8Async, w) &&
            sym(h, "cuGetErrorString", d.cuGetErrorString, w) &&
-           sym(h, "cuFuncSetAttribute", d.cuFuncSetAttribute, w);
+           sym(h, "cuFuncSetAttribute", d.cuFuncSetAttribute, w) && sym(h, "cuEventRecord", d.cuEventRecord, w);
     if (d.ok && d.cuInit(0) != 0) {
       d.ok = false;
       d.why = "cuInit failed (no usable GPU)";
@@ -189,6 +190,12 @@ struct canvas_plan {
   std::vector<SizeRule> saved, ws;
   std::vector<Record> recs;
   std::vector<CUfunction> fns;
+  // measurement hook (canvas_plan_profile): CUDA events recorded around every
+  // launch of one record, so bench.py can time one kernel inside a full step
+  mutable std::mutex prof_mu;
+  int64_t prof_record = -1;
+  std::vector<void*> prof_events;  // 2 per slot: start, end
+  mutable int64_t prof_count = 0;
 };
 
 namespace {
@@ -322,9 +329,18 @@ int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, co
       unsigned g[3];
       for (int i = 0; i < 3; ++i) g[i] = (unsigned)r.grid[i].eval(batch);
       void* params[] = {&a};
+      void* ev_end = nullptr;
+      const int64_t ri = &r - p->recs.data();
+      if (ri == p->prof_record && !p->prof_events.empty()) {
+        std::lock_guard<std::mutex> lk(p->prof_mu);
+        const size_t slot = (size_t)(p->prof_count++ % (int64_t)(p->prof_events.size() / 2));
+        d.cuEventRecord(p->prof_events[2 * slot], st);
+        ev_end = p->prof_events[2 * slot + 1];
+      }
       CUresult e = d.cuLaunchKernel(p->fns[r.kernel], g[0], g[1], g[2], (unsigned)r.block, 1, 1, 0, st, params,
                                     nullptr);
       if (e != 0) return fail(CANVAS_ERR_CUDA, "launch kernel " + std::to_string(r.kernel) + ": " + cu_err(e));
+      if (ev_end) d.cuEventRecord(ev_end, st);
     }
   }
   return CANVAS_OK;
@@ -459,6 +475,18 @@ int canvas_plan_launches(const canvas_plan* p, int phase) {
     if (r.phase == phase && r.kind == 0) n += (int)p->copies;
   return n;
 }
+
+int canvas_plan_profile(canvas_plan* p, int record, void* const* events, int n_pairs) {
+  if (!p || record >= (int)p->recs.size() || n_pairs < 0 || (n_pairs && !events))
+    return fail(CANVAS_ERR_ARGS, "bad profile request");
+  std::lock_guard<std::mutex> lk(p->prof_mu);
+  p->prof_record = record;
+  p->prof_events.assign(events, events + 2 * n_pairs);
+  p->prof_count = 0;
+  return CANVAS_OK;
+}
+
+int64_t canvas_plan_profile_count(const canvas_plan* p) { return p ? p->prof_count : -1; }
 
 int canvas_forward(const canvas_plan* p, int64_t batch, const float* x, const float* const* fc_w, int n_fc, float* y,
                    void* saved, void* workspace, void* stream) {

@@ -75,6 +75,9 @@ def load_library() -> ctypes.CDLL:
         lib.canvas_plan_query.argtypes = [c.c_void_p, c.c_int64, c.POINTER(c.c_size_t), c.POINTER(c.c_size_t), c.POINTER(c.c_size_t)]
         lib.canvas_plan_launches.argtypes = [c.c_void_p, c.c_int]
         lib.canvas_forward.argtypes = [c.c_void_p, c.c_int64, c.c_void_p, c.c_void_p, c.c_int, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p]
+        lib.canvas_plan_profile.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int]
+        lib.canvas_plan_profile_count.argtypes = [c.c_void_p]
+        lib.canvas_plan_profile_count.restype = c.c_int64
         lib.canvas_backward.argtypes = [c.c_void_p, c.c_int64, c.c_void_p, c.c_void_p, c.c_int, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p]
         _lib = lib
         return lib
@@ -115,6 +118,24 @@ class DevicePlan:
 
     def launches(self, phase: int) -> int:
         return self.lib.canvas_plan_launches(self.handle, phase)
+
+    def record_index(self, pattern: str) -> int:
+        """Index of the first launch record whose kernel name contains ``pattern``."""
+        for i, L in enumerate(self.plan.launches):
+            if L.kind == "kernel" and pattern in L.name:
+                return i
+        raise KeyError(pattern)
+
+    def profile(self, record: int, events) -> None:
+        """Record ``events`` (list of (start, end) torch.cuda.Event) around launches of ``record``."""
+        arr = (ctypes.c_void_p * max(1, 2 * len(events)))()
+        for i, (a, b) in enumerate(events):
+            arr[2 * i] = a.cuda_event
+            arr[2 * i + 1] = b.cuda_event
+        _check(self.lib.canvas_plan_profile(self.handle, record, arr, len(events)))
+
+    def profile_count(self) -> int:
+        return self.lib.canvas_plan_profile_count(self.handle)
 
     @staticmethod
     def _ptr_array(tensors) -> ctypes.Array:
