@@ -1,0 +1,67 @@
+"""Lowering correctness on the CPU: generated functors + launch schedule run
+through the host emulator (tests/emu) vs the fp64 oracle, same tolerances as
+the GPU parity tests.  Covers every pinned kernel, Fig.-2 replication (concat
+and sum) with the stride-2 policy, and ALL 256 kernels of the reference
+sampler sweep (nodes=10, seed=7; 48 with free variables)."""
+
+import multiprocessing
+import os
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+import pytest
+
+from emu.runner import EmuPlan
+from paper_2304_07741_b200 import zoo
+from parity import assert_close, reference
+
+
+def emu_run(case):
+    ep = EmuPlan(case.plan)
+    flat = [w.float().numpy().copy() for c in case.weights for w in c]
+    x = case.x.float().numpy().copy()
+    y, saved = ep.forward(x, flat)
+    dx, dws = ep.backward(x, flat, saved, case.dy.float().numpy().copy())
+    return y, dx, dws
+
+
+@pytest.mark.parametrize("name", list(zoo.ALL))
+def test_pinned(name):
+    case = reference(zoo.ALL[name], 16, 16, 10, 9)
+    assert_close(case, *emu_run(case), name)
+
+
+@pytest.mark.parametrize("cin,cout,stride", [(8, 16, 2), (16, 8, 1), (8, 32, 2)])
+@pytest.mark.parametrize("name", ["seed7_k1", "involution", "seed7_k0"])
+def test_replication(name, cin, cout, stride):
+    case = reference(zoo.ALL[name], cin, cout, 9, 10, stride=stride, n=2)
+    assert_close(case, *emu_run(case), f"{name} {cin}->{cout} s{stride}")
+
+
+def _one(i):
+    import torch
+
+    torch.set_num_threads(1)
+    texts = ["canvas-ir v1\n" + t for t in open("tests/golden/sampler_10_7_256.cir").read().split("canvas-ir v1\n")[1:]]
+    case = reference(texts[i], 16, 16, 8, 8)
+    try:
+        assert_close(case, *emu_run(case), f"sweep #{i}")
+    except AssertionError as e:
+        return str(e)
+    return None
+
+
+def test_sampler_sweep_256():
+    with ProcessPoolExecutor(min(8, os.cpu_count() or 1), mp_context=multiprocessing.get_context("spawn")) as ex:
+        errs = [e for e in ex.map(_one, range(256)) if e]
+    assert not errs, errs[:5]
+
+
+def test_blob_roundtrip_fields():
+    from paper_2304_07741_b200.executor import plan_for
+
+    p = plan_for(zoo.SEED7_K1, c_in=64, c_out=128, h=56, w=56, stride=2)
+    b = p.blob()
+    assert b[:8] == b"CNVSBLOB"
+    assert p.copies == 2 and p.mode == "concat" and p.y_copy_off == 64 * 28 * 28
+    assert np.frombuffer(b[8:16], np.int64)[0] == 1
