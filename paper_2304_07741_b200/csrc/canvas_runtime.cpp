@@ -165,7 +165,7 @@ struct GridRule {
 };
 constexpr int kMaxSlots = 24;
 struct Record {
-  int64_t kind, phase, kernel, block;
+  int64_t kind, phase, kernel, block, smem;
   GridRule grid[3];
   int64_t nslots;
   int64_t slots[kMaxSlots];
@@ -337,7 +337,7 @@ int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, co
         d.cuEventRecord(p->prof_events[2 * slot], st);
         ev_end = p->prof_events[2 * slot + 1];
       }
-      CUresult e = d.cuLaunchKernel(p->fns[r.kernel], g[0], g[1], g[2], (unsigned)r.block, 1, 1, 0, st, params,
+      CUresult e = d.cuLaunchKernel(p->fns[r.kernel], g[0], g[1], g[2], (unsigned)r.block, 1, 1, (unsigned)r.smem, st, params,
                                     nullptr);
       if (e != 0) return fail(CANVAS_ERR_CUDA, "launch kernel " + std::to_string(r.kernel) + ": " + cu_err(e));
       if (ev_end) d.cuEventRecord(ev_end, st);
@@ -400,6 +400,7 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
     r.phase = rd.i64();
     r.kernel = rd.i64();
     r.block = rd.i64();
+    r.smem = rd.i64();
     for (auto& g : r.grid) g = GridRule{rd.i64(), rd.i64(), rd.i64(), rd.i64()};
     r.nslots = rd.i64();
     for (auto& s : r.slots) s = rd.i64();
@@ -449,6 +450,12 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
     e = d.cuModuleGetFunction(&f, mod, nm.c_str());
     if (e != 0) return fail(CANVAS_ERR_CUDA, "cuModuleGetFunction(" + nm + "): " + cu_err(e));
     p->fns.push_back(f);
+  }
+  for (const Record& r : p->recs) {
+    if (r.kind == 0 && r.smem > 48 * 1024) {
+      e = d.cuFuncSetAttribute(p->fns[r.kernel], 8 /* MAX_DYNAMIC_SHARED_SIZE_BYTES */, (int)r.smem);
+      if (e != 0) return fail(CANVAS_ERR_CUDA, "cuFuncSetAttribute(smem " + std::to_string(r.smem) + "): " + cu_err(e));
+    }
   }
   *out = p.release();
   return CANVAS_OK;

@@ -27,6 +27,7 @@
 #endif
 
 #define CANVAS_MAX_KSLOTS 24
+typedef unsigned char uint8_t;
 
 struct CanvasArgs {
   float* p[CANVAS_MAX_KSLOTS];  // tensors this launch touches (plan slot table)
@@ -188,6 +189,406 @@ __device__ __forceinline__ void reduce_partials(const CanvasArgs& a) {
     float s = 0.f;
     for (int z = 0; z < Z; ++z) s += P[(long long)z * F::MJ + idx];
     out[idx] = s;
+  }
+}
+
+
+// ===========================================================================
+// K3 (tensor cores): tcgen05 3xTF32 GEMMs with a computed operand.
+//
+// The FC contraction runs on the 5th-gen tensor cores in split precision:
+// x = hi + lo with hi = rna_tf32(x), lo = rna_tf32(x - hi), and
+// D += A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in fp32 in TMEM, which
+// meets fp32 tolerance where plain TF32 fails (SURVEY §7 decision 4).
+//
+// Warp roles (288 threads): warps 0-7 are producers — they evaluate the
+// functor operands (the fused producer chain of the FC input: unfold /
+// shift / group index maps and pointwise ops folded into the loads), split
+// them, and store them into a STAGES-deep ring of 128B-swizzled K-major smem
+// tiles (the canonical UMMA layout, 1024 B atoms); warp 8 allocates TMEM and
+// one elected lane issues tcgen05.mma (M=128, N=NT, K=8 per instruction) and
+// tcgen05.commit back to the producers; after the last k-block warps 0-7
+// drain TMEM with tcgen05.ld (warp w reads lane quadrant w%4, column half w/4)
+// and run the functor's store epilogue.
+// ===========================================================================
+typedef unsigned int cv_u32;
+typedef unsigned long long cv_u64;
+
+namespace tc {
+
+__device__ __forceinline__ cv_u32 smem_u32(const void* p) {
+  return (cv_u32)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(cv_u64* bar, cv_u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(cv_u64* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(cv_u64* bar, cv_u32 parity) {
+  const cv_u32 a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// split x into (hi, lo) tf32 bit patterns
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  cv_u32 h, l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
+}
+
+__device__ __forceinline__ void st_shared_v4(void* p, float a, float b, float c, float d) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
+// K-major, 128B-swizzle smem descriptor (rows of 128 B, 8-row atoms 1024 B apart)
+__device__ __forceinline__ cv_u64 desc_k_sw128(cv_u32 saddr) {
+  cv_u64 d = 0;
+  d |= (cv_u64)((saddr >> 4) & 0x3FFF);
+  d |= (cv_u64)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (cv_u64)(1024 >> 4) << 32;       // SBO: 8 rows x 128 B
+  d |= (cv_u64)1 << 46;                 // descriptor version (sm_100)
+  d |= (cv_u64)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: kind::tf32, D fp32, A/B K-major, M=128, N=n
+__host__ __device__ constexpr cv_u32 idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((cv_u32)(n >> 3) << 17) | ((cv_u32)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(cv_u32 dtmem, cv_u64 adesc, cv_u64 bdesc, cv_u32 idesc, cv_u32 accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+__device__ __forceinline__ void commit(cv_u64* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int NCOLS>
+__device__ __forceinline__ void tmem_alloc(cv_u32* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "n"(NCOLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int NCOLS>
+__device__ __forceinline__ void tmem_free(cv_u32 taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(NCOLS));
+}
+
+__device__ __forceinline__ void tmem_ld16(cv_u32 taddr, float* v) {
+  cv_u32 r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+template <int N>
+struct TmemCols {
+  static constexpr int value = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
+};
+
+constexpr int kProducerWarps = 8;
+constexpr int kThreads = (kProducerWarps + 1) * 32;
+constexpr int kBM = 128;  // MMA rows per tile
+constexpr int kBK = 32;   // tf32 per 128 B swizzle row = one k-block
+
+// swizzled byte offset of 16 B chunk c (0..7) of row r in a K-major SW128 tile
+__device__ __forceinline__ int swz(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+// Shared memory plan of one pipeline: STAGES x {A_hi, A_lo, B_hi, B_lo} + barriers.
+template <int NT, int STAGES>
+struct Smem {
+  static constexpr int A_BYTES = kBM * 128;
+  static constexpr int B_BYTES = NT * 128;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;  // + alignment slack
+};
+
+// MMA issuer: consumes STAGES-deep ring, 3 MMAs per K=8 step (hi.hi, hi.lo, lo.hi)
+template <int NT, int STAGES>
+__device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* empty, cv_u64* done, cv_u32 tmem, int KB) {
+  using L = Smem<NT, STAGES>;
+  constexpr cv_u32 idesc = idesc_tf32(NT);
+  for (int kb = 0; kb < KB; ++kb) {
+    const int st = kb % STAGES;
+    mbar_wait(&full[st], (kb / STAGES) & 1);
+    fence_after();
+    const cv_u32 a_hi = smem_u32(smem + st * L::STAGE);
+    const cv_u32 a_lo = a_hi + L::A_BYTES;
+    const cv_u32 b_hi = a_lo + L::A_BYTES;
+    const cv_u32 b_lo = b_hi + L::B_BYTES;
+#pragma unroll
+    for (int kk = 0; kk < kBK / 8; ++kk) {
+      const cv_u32 o = kk * 32;  // 8 tf32 = 32 B along K inside the swizzled row
+      mma_tf32(tmem, desc_k_sw128(a_hi + o), desc_k_sw128(b_hi + o), idesc, (kb | kk) != 0);
+      mma_tf32(tmem, desc_k_sw128(a_hi + o), desc_k_sw128(b_lo + o), idesc, 1);
+      mma_tf32(tmem, desc_k_sw128(a_lo + o), desc_k_sw128(b_hi + o), idesc, 1);
+    }
+    commit(&empty[st]);
+  }
+  commit(done);
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+// FC forward / dgrad on tensor cores: out[n][m][s] = sum_k A(m,k) B(n,k,s),
+// MMA rows = 128 pixels t = n*S + s (operand B(n,k,s), computed), MMA cols =
+// NT output channels (operand A(m,k), weights).
+// ---------------------------------------------------------------------------
+template <class F, int NT, int STAGES>
+__device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
+  using namespace tc;
+  using L = Smem<NT, STAGES>;
+  constexpr int NCOLS = TmemCols<NT>::value;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((unsigned long long)smem_raw + 1023) & ~1023ull);
+  cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
+  cv_u64* empty = full + STAGES;
+  cv_u64* done = empty + STAGES;
+  cv_u32* tslot = (cv_u32*)(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int KB = (F::K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], kProducerWarps * 32);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProducerWarps) tmem_alloc<NCOLS>(tslot);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const cv_u32 tmem = *tslot;
+
+  const long long T = a.n * (long long)F::S;
+  const long long t0 = (long long)blockIdx.x * kBM;
+  const int c0 = blockIdx.y * NT;
+
+  if (warp < kProducerWarps) {
+    const int p = threadIdx.x;          // 0..255
+    const int r = p & (kBM - 1);        // tile row (pixel)
+    const int half = p >> 7;            // chunks [4*half, 4*half+4)
+    const long long t = t0 + r;
+    const bool ok = t < T;
+    const long long n = ok ? t / F::S : 0;
+    const int s = ok ? (int)(t - n * F::S) : 0;
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* sa_hi = smem + st * L::STAGE;
+      uint8_t* sa_lo = sa_hi + L::A_BYTES;
+      uint8_t* sb_hi = sa_lo + L::A_BYTES;
+      uint8_t* sb_lo = sb_hi + L::B_BYTES;
+      const int kbase = kb * kBK;
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        const int c = half * 4 + cc;
+        float v[4], h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int k = kbase + c * 4 + j;
+          v[j] = (ok && k < F::K) ? F::B(a, n, k, s) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
+        const int off = swz(r, c);
+        st_shared_v4(sa_hi + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(sa_lo + off, l[0], l[1], l[2], l[3]);
+      }
+      for (int row = r; row < NT; row += kBM) {
+        const int col = c0 + row;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          const int c = half * 4 + cc;
+          float v[4], h[4], l[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int k = kbase + c * 4 + j;
+            v[j] = (col < F::M && k < F::K) ? F::A(a, col, k) : 0.f;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
+          const int off = swz(row, c);
+          st_shared_v4(sb_hi + off, h[0], h[1], h[2], h[3]);
+          st_shared_v4(sb_lo + off, l[0], l[1], l[2], l[3]);
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(&full[st]);
+    }
+    // epilogue: TMEM lane quadrant = warp % 4, column half = warp / 4
+    mbar_wait(done, 0);
+    fence_after();
+    const int q = warp & 3;
+    const int tr = q * 32 + lane;  // accumulator row owned by this thread
+    const long long te = t0 + tr;
+    const bool eok = te < T;
+    const long long en = eok ? te / F::S : 0;
+    const int es = eok ? (int)(te - en * F::S) : 0;
+    constexpr int HALF = ((NT + 31) / 32) * 16;  // columns per warpgroup, multiple of 16
+    const int cbeg = (warp >> 2) * HALF;
+    for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + cc, v);
+      if (eok) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int col = c0 + cc + j;
+          if (cc + j < NT && col < F::M) F::store(a, en, col, es, v[j]);
+        }
+      }
+    }
+  } else if (lane == 0) {
+    mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kProducerWarps) {
+    fence_after();
+    tmem_free<NCOLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FC wgrad on tensor cores: P[z][m][j] = sum_{t in chunk z} A(n,m,s) B(n,j,s).
+// MMA rows = 128 input channels j (operand B), MMA cols = NT output channels
+// m (operand A), reduction over a TCHUNK slice of pixels t; partials are
+// summed in order by reduce_partials (deterministic).
+// ---------------------------------------------------------------------------
+template <class F, int NT, int STAGES>
+__device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
+  using namespace tc;
+  using L = Smem<NT, STAGES>;
+  constexpr int NCOLS = TmemCols<NT>::value;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((unsigned long long)smem_raw + 1023) & ~1023ull);
+  cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
+  cv_u64* empty = full + STAGES;
+  cv_u64* done = empty + STAGES;
+  cv_u32* tslot = (cv_u32*)(done + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], kProducerWarps * 32);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kProducerWarps) tmem_alloc<NCOLS>(tslot);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const cv_u32 tmem = *tslot;
+
+  const long long T = a.n * (long long)F::S;
+  const long long tbeg = (long long)blockIdx.z * F::TCHUNK;
+  const long long tend = tbeg + F::TCHUNK < T ? tbeg + F::TCHUNK : T;
+  const int KB = (int)((tend - tbeg + kBK - 1) / kBK);
+  const int j0 = blockIdx.x * kBM;  // rows: input channels
+  const int m0 = blockIdx.y * NT;   // cols: output channels
+
+  if (warp < kProducerWarps) {
+    const int p = threadIdx.x;  // 0..255
+    const int c = p & 7;        // 16 B chunk = 4 consecutive pixels
+    const int rsub = p >> 3;    // 0..31: row within a 32-row pass
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* sa_hi = smem + st * L::STAGE;
+      uint8_t* sa_lo = sa_hi + L::A_BYTES;
+      uint8_t* sb_hi = sa_lo + L::A_BYTES;
+      uint8_t* sb_lo = sb_hi + L::B_BYTES;
+      long long nn[4];
+      int ss[4];
+      bool okk[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const long long t = tbeg + (long long)kb * kBK + c * 4 + j;
+        okk[j] = t < tend;
+        nn[j] = okk[j] ? t / F::S : 0;
+        ss[j] = okk[j] ? (int)(t - nn[j] * F::S) : 0;
+      }
+      for (int row = rsub; row < kBM; row += 32) {
+        const int jj = j0 + row;
+        float v[4], h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (okk[j] && jj < F::J) ? F::B(a, nn[j], jj, ss[j]) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
+        const int off = swz(row, c);
+        st_shared_v4(sa_hi + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(sa_lo + off, l[0], l[1], l[2], l[3]);
+      }
+      for (int row = rsub; row < NT; row += 32) {
+        const int mm = m0 + row;
+        float v[4], h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = (okk[j] && mm < F::M) ? F::A(a, nn[j], mm, ss[j]) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
+        const int off = swz(row, c);
+        st_shared_v4(sb_hi + off, h[0], h[1], h[2], h[3]);
+        st_shared_v4(sb_lo + off, l[0], l[1], l[2], l[3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&full[st]);
+    }
+    mbar_wait(done, 0);
+    fence_after();
+    const int q = warp & 3;
+    const int jj = j0 + q * 32 + lane;
+    float* P = F::partials(a) + (long long)blockIdx.z * F::M * F::J;
+    constexpr int HALF = ((NT + 31) / 32) * 16;
+    const int cbeg = (warp >> 2) * HALF;
+    for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {
+      float v[16];
+      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + cc, v);
+      if (jj < F::J) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int mm = m0 + cc + j;
+          if (cc + j < NT && mm < F::M) P[(long long)mm * F::J + jj] = KB > 0 ? v[j] : 0.f;
+        }
+      }
+    }
+  } else if (lane == 0) {
+    if (KB > 0) mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
+    else tc::mbar_arrive(done);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == kProducerWarps) {
+    fence_after();
+    tmem_free<NCOLS>(tmem);
   }
 }
 

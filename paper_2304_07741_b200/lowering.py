@@ -51,6 +51,23 @@ POINTWISE_BLOCK = 256
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
 GEMM_TILE = 64
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
+TC_THREADS = 288  # tcgen05 GEMM: 8 producer/epilogue warps + 1 MMA warp
+TC_SMEM_BUDGET = 200 * 1024
+TC_WGRAD_TCHUNK = 4096  # pixels per wgrad split (128 k-blocks of 32)
+
+
+def tc_tile(cols: int) -> tuple[int, int, int]:
+    """(NT, number of column tiles, pipeline stages) for an MMA N extent of ``cols``."""
+    nct = -(-cols // 256)
+    nt = -(-(-(-cols // nct)) // 16) * 16
+    stage = 2 * 128 * 128 + 2 * nt * 128
+    stages = max(2, min(4, TC_SMEM_BUDGET // stage))
+    return nt, nct, stages
+
+
+def tc_smem_bytes(nt: int, stages: int) -> int:
+    """Must match canvas::tc::Smem<NT, STAGES>::BYTES."""
+    return stages * (2 * 128 * 128 + 2 * nt * 128) + (2 * stages + 1) * 8 + 16 + 1024
 
 
 @dataclass
@@ -102,6 +119,7 @@ class Launch:
     beta: int = BETA_NONE
     memset_slot: int = -1
     memset_size: SizeRule | None = None
+    smem: int = 0  # dynamic shared memory bytes
     what: str = ""  # human-readable role (profiles / DESIGN tables)
     bytes_per_image: int = 0  # algorithmic HBM bytes per image (roofline)
     flops_per_image: int = 0  # useful FLOPs per image (2 per MAC)
@@ -152,7 +170,7 @@ class Plan:
         header: magic[8], then int64s: version, n_kernels, n_launches, n_saved,
         n_ws, n_fc, copies, x_copy_off, y_copy_off, dx_copy_off, dy_copy_off,
         src_len, names_len; then (a_num, a_den, b) per saved and per ws slot;
-        then per launch: kind, phase, kernel, block, 3x(a,b,d,cap), nslots,
+        then per launch: kind, phase, kernel, block, smem, 3x(a,b,d,cap), nslots,
         slots[MAX_KSLOTS], beta, memset_slot, memset (a_num,a_den,b); then the
         CUDA source and the NUL-separated kernel names.
         """
@@ -169,7 +187,7 @@ class Plan:
             grid = list(L.grid) if L.grid else [GridRule(0, 1, 1)] * 3
             slots = list(L.slots) + [-1] * (MAX_KSLOTS - len(L.slots))
             ms = L.memset_size or SizeRule(0, 1, 0)
-            out += struct.pack("<4q", 0 if L.kind == "kernel" else 1, L.phase, L.kernel, L.block)
+            out += struct.pack("<5q", 0 if L.kind == "kernel" else 1, L.phase, L.kernel, L.block, L.smem)
             for g in grid:
                 out += struct.pack("<4q", g.a, g.b, g.d, g.cap)
             out += struct.pack("<q", len(L.slots))
@@ -331,7 +349,8 @@ class Fn:
 class Lowerer:
     """Builds a :class:`Plan` for one concrete graph and replacement target."""
 
-    def __init__(self, g: ConcreteGraph, plan: Plan):
+    def __init__(self, g: ConcreteGraph, plan: Plan, use_tc: bool = True):
+        self.use_tc = use_tc
         self.g = g
         self.p = plan
         self.nodes = g.nodes
@@ -807,6 +826,14 @@ class Lowerer:
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }", "};"]
         functor = "\n".join(lines) + "\n"
+        if self.use_tc and M >= 8 and K >= 16:
+            nt, nct, stages = tc_tile(M)
+            smem = tc_smem_bytes(nt, stages)
+            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, 1) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}>(a); }}\n'
+            k = self.add_kernel(name, functor, launcher)
+            grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
+            self.p.launches.append(Launch("kernel", phase, name, k, TC_THREADS, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+            return
         launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_nk<{name}_F>(a); }}\n'
         k = self.add_kernel(name, functor, launcher)
         grid = (GridRule(S, 0, GEMM_TILE), GridRule(0, M, GEMM_TILE), GridRule(0, 1, 1))
@@ -814,7 +841,8 @@ class Lowerer:
 
     def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops) -> None:
         """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
-        tchunk = max(2048, -(-4096 * S // 60000) * GEMM_TILE)
+        use_tc = self.use_tc and J >= 32 and M >= 8
+        tchunk = TC_WGRAD_TCHUNK if use_tc else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
         self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
         fa, fb = Fn(self), Fn(self)
@@ -835,10 +863,18 @@ class Lowerer:
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
         lines += ["};"]
         functor = "\n".join(lines) + "\n"
-        launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_wgrad<{name}_F>(a); }}\n'
-        k = self.add_kernel(name, functor, launcher)
-        grid = (GridRule(0, J, GEMM_TILE), GridRule(0, M, GEMM_TILE), GridRule(S, 0, tchunk))
-        self.p.launches.append(Launch("kernel", 1, name, k, 256, grid, tuple(fa.local_slots), BETA_NONE, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+        if use_tc:
+            nt, nct, stages = tc_tile(M)
+            smem = tc_smem_bytes(nt, stages)
+            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, 1) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}>(a); }}\n'
+            k = self.add_kernel(name, functor, launcher)
+            grid = (GridRule(0, J, 128), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
+            self.p.launches.append(Launch("kernel", 1, name, k, TC_THREADS, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+        else:
+            launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_wgrad<{name}_F>(a); }}\n'
+            k = self.add_kernel(name, functor, launcher)
+            grid = (GridRule(0, J, GEMM_TILE), GridRule(0, M, GEMM_TILE), GridRule(S, 0, tchunk))
+            self.p.launches.append(Launch("kernel", 1, name, k, 256, grid, tuple(fa.local_slots), BETA_NONE, what=what, bytes_per_image=nbytes, flops_per_image=flops))
         # ordered reduction of the partials into dW
         rname = name + "_reduce"
         rsrc = (
@@ -1004,7 +1040,7 @@ class Lowerer:
         del nsv
 
 
-def lower(g: ConcreteGraph, *, c_in: int, c_out: int, stride: int = 1, h_in: int | None = None, w_in: int | None = None) -> Plan:
+def lower(g: ConcreteGraph, *, c_in: int, c_out: int, stride: int = 1, h_in: int | None = None, w_in: int | None = None, use_tc: bool = True) -> Plan:
     """Build the fwd+bwd plan of one replacement target (SPEC.md:417-425 Fig.-2, App. A.10).
 
     ``g`` is evaluated at C = min(c_in, c_out) and the *output* resolution;
@@ -1029,7 +1065,7 @@ def lower(g: ConcreteGraph, *, c_in: int, c_out: int, stride: int = 1, h_in: int
     else:
         p.x_copy_off = c * hw_in
         p.dx_copy_off = c * hw_in
-    lw = Lowerer(g, p)
+    lw = Lowerer(g, p, use_tc)
     lw.lower_forward()
     lw.lower_backward()
     lw.finish()

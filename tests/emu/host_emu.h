@@ -87,4 +87,8 @@ void reduce_partials(const CanvasArgs& a) {
     a.p[1][idx] = s;
   }
 }
+template <class F, int NT, int STAGES>
+void tc_gemm_pix(const CanvasArgs& a) { gemm_nk<F>(a); }
+template <class F, int NT, int STAGES>
+void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 }  // namespace canvas
