@@ -235,6 +235,16 @@ __device__ __forceinline__ void mbar_wait(cv_u64* bar, cv_u32 parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_tx(cv_u64* bar, cv_u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// TMA bulk copy (1-D) global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, cv_u32 bytes, cv_u64* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -310,7 +320,7 @@ struct TmemCols {
 };
 
 constexpr int kProducerWarps = 8;
-constexpr int kThreads = (kProducerWarps + 1) * 32;
+constexpr int kThreads = (kProducerWarps + 2) * 32;  // + MMA warp + bulk-copy warp
 constexpr int kBM = 128;  // MMA rows per tile
 constexpr int kBK = 32;   // tf32 per 128 B swizzle row = one k-block
 
@@ -359,7 +369,7 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
 // MMA rows = 128 pixels t = n*S + s (operand B(n,k,s), computed), MMA cols =
 // NT output channels (operand A(m,k), weights).
 // ---------------------------------------------------------------------------
-template <class F, int NT, int STAGES>
+template <class F, int NT, int STAGES, bool PACKED>
 __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   using namespace tc;
   using L = Smem<NT, STAGES>;
@@ -375,7 +385,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], kProducerWarps * 32);
+      mbar_init(&full[i], kProducerWarps * 32 + (PACKED ? 1 : 0));
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
@@ -394,11 +404,38 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   if (warp < kProducerWarps) {
     const int p = threadIdx.x;          // 0..255
     const int r = p & (kBM - 1);        // tile row (pixel)
-    const int half = p >> 7;            // chunks [4*half, 4*half+4)
+    const int half = p >> 7;            // 16 k of the 32-wide k-block
     const long long t = t0 + r;
     const bool ok = t < T;
     const long long n = ok ? t / F::S : 0;
     const int s = ok ? (int)(t - n * F::S) : 0;
+    constexpr int WR = PACKED ? 0 : (NT + kBM - 1) / kBM;  // weight rows per thread (unpacked path)
+    float va[16], vb[WR > 0 ? WR : 1][16];
+    // Gather one k-block into registers: every address is clamped in range, the
+    // value selected afterwards, so all loads issue back to back (no branches)
+    // and overlap the wait for the ring slot.
+    auto gather = [&](int kb) {
+      const int kbase = kb * kBK + half * 16;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = kbase + i;
+        const float v = F::B(a, n, k < F::K ? k : F::K - 1, s);
+        va[i] = (ok && k < F::K) ? v : 0.f;
+      }
+#pragma unroll
+      for (int w = 0; w < WR; ++w) {
+        const int row = r + w * kBM;
+        const int col = c0 + row;
+        const int cl = col < F::M ? col : F::M - 1;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int k = kbase + i;
+          const float v = F::A(a, cl, k < F::K ? k : F::K - 1);
+          vb[w][i] = (row < NT && col < F::M && k < F::K) ? v : 0.f;
+        }
+      }
+    };
+    gather(0);
     for (int kb = 0; kb < KB; ++kb) {
       const int st = kb % STAGES;
       if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
@@ -406,42 +443,33 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       uint8_t* sa_lo = sa_hi + L::A_BYTES;
       uint8_t* sb_hi = sa_lo + L::A_BYTES;
       uint8_t* sb_lo = sb_hi + L::B_BYTES;
-      const int kbase = kb * kBK;
 #pragma unroll
       for (int cc = 0; cc < 4; ++cc) {
-        const int c = half * 4 + cc;
-        float v[4], h[4], l[4];
+        float h[4], l[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int k = kbase + c * 4 + j;
-          v[j] = (ok && k < F::K) ? F::B(a, n, k, s) : 0.f;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
-        const int off = swz(r, c);
-        st_shared_v4(sa_hi + off, h[0], h[1], h[2], h[3]);
-        st_shared_v4(sa_lo + off, l[0], l[1], l[2], l[3]);
+        for (int j = 0; j < 4; ++j) split_tf32(va[cc * 4 + j], h[j], l[j]);
+        const int off = swz(r, half * 4 + cc);
+        *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
       }
-      for (int row = r; row < NT; row += kBM) {
-        const int col = c0 + row;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          const int c = half * 4 + cc;
-          float v[4], h[4], l[4];
+      for (int w = 0; w < WR; ++w) {
+        const int row = r + w * kBM;
+        if (row < NT) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int k = kbase + c * 4 + j;
-            v[j] = (col < F::M && k < F::K) ? F::A(a, col, k) : 0.f;
+          for (int cc = 0; cc < 4; ++cc) {
+            float h[4], l[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) split_tf32(vb[w][cc * 4 + j], h[j], l[j]);
+            const int off = swz(row, half * 4 + cc);
+            *reinterpret_cast<float4*>(sb_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+            *reinterpret_cast<float4*>(sb_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
           }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
-          const int off = swz(row, c);
-          st_shared_v4(sb_hi + off, h[0], h[1], h[2], h[3]);
-          st_shared_v4(sb_lo + off, l[0], l[1], l[2], l[3]);
         }
       }
       fence_async_smem();
       mbar_arrive(&full[st]);
+      if (kb + 1 < KB) gather(kb + 1);
     }
     // epilogue: TMEM lane quadrant = warp % 4, column half = warp / 4
     mbar_wait(done, 0);
@@ -465,14 +493,54 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         }
       }
     }
-  } else if (lane == 0) {
-    mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
+  } else if (warp == kProducerWarps) {
+    if (lane == 0) mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
+  } else if (PACKED && lane == 0) {
+    // B operand: pre-split, pre-swizzled weight tile images (tc_pack_b), one
+    // TMA bulk copy of {hi, lo} per k-block
+    const uint8_t* img = reinterpret_cast<const uint8_t*>(F::packed(a)) + (long long)blockIdx.y * KB * 2 * L::B_BYTES;
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* sb_hi = smem + st * L::STAGE + 2 * L::A_BYTES;
+      mbar_arrive_tx(&full[st], 2 * L::B_BYTES);
+      bulk_g2s(sb_hi, img + (long long)kb * 2 * L::B_BYTES, 2 * L::B_BYTES, &full[st]);
+    }
   }
   fence_before();
   __syncthreads();
   if (warp == kProducerWarps) {
     fence_after();
     tmem_free<NCOLS>(tmem);
+  }
+}
+
+// Pack the weight operand A(m,k) of a tc_gemm_pix launch into per-(column tile,
+// k-block) images of the swizzled smem layout: [hi NT x 128 B][lo NT x 128 B],
+// so the GEMM streams them with TMA bulk copies instead of per-row gathers.
+template <class F, int NT>
+__device__ __forceinline__ void tc_pack_b(const CanvasArgs& a) {
+  constexpr int KB = (F::K + tc::kBK - 1) / tc::kBK;
+  constexpr int NCT = (F::M + NT - 1) / NT;
+  constexpr int BB = NT * 128;
+  constexpr long long TOTAL = (long long)NCT * KB * NT * tc::kBK;
+  float* img = F::packed(a);
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < TOTAL; i += (long long)gridDim.x * blockDim.x) {
+    const int kk = (int)(i % tc::kBK);
+    const long long rest = i / tc::kBK;
+    const int row = (int)(rest % NT);
+    const long long tile = rest / NT;  // ct * KB + kb
+    const int kb = (int)(tile % KB);
+    const int ct = (int)(tile / KB);
+    const int col = ct * NT + row;
+    const int k = kb * tc::kBK + kk;
+    const float v = (col < F::M && k < F::K) ? F::A(a, col, k) : 0.f;
+    float hi, lo;
+    tc::split_tf32(v, hi, lo);
+    uint8_t* base = reinterpret_cast<uint8_t*>(img) + tile * 2 * BB;
+    const int off = tc::swz(row, kk >> 2) + (kk & 3) * 4;
+    *reinterpret_cast<float*>(base + off) = hi;
+    *reinterpret_cast<float*>(base + BB + off) = lo;
   }
 }
 
@@ -520,13 +588,9 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     const int p = threadIdx.x;  // 0..255
     const int c = p & 7;        // 16 B chunk = 4 consecutive pixels
     const int rsub = p >> 3;    // 0..31: row within a 32-row pass
-    for (int kb = 0; kb < KB; ++kb) {
-      const int st = kb % STAGES;
-      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
-      uint8_t* sa_hi = smem + st * L::STAGE;
-      uint8_t* sa_lo = sa_hi + L::A_BYTES;
-      uint8_t* sb_hi = sa_lo + L::A_BYTES;
-      uint8_t* sb_lo = sb_hi + L::B_BYTES;
+    constexpr int RA = kBM / 32, RB = (NT + 31) / 32;
+    float va[RA][4], vb[RB][4];
+    auto gather = [&](int kb) {
       long long nn[4];
       int ss[4];
       bool okk[4];
@@ -534,33 +598,63 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       for (int j = 0; j < 4; ++j) {
         const long long t = tbeg + (long long)kb * kBK + c * 4 + j;
         okk[j] = t < tend;
-        nn[j] = okk[j] ? t / F::S : 0;
-        ss[j] = okk[j] ? (int)(t - nn[j] * F::S) : 0;
+        const long long tc = okk[j] ? t : tbeg;
+        nn[j] = tc / F::S;
+        ss[j] = (int)(tc - nn[j] * F::S);
       }
-      for (int row = rsub; row < kBM; row += 32) {
-        const int jj = j0 + row;
-        float v[4], h[4], l[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = (okk[j] && jj < F::J) ? F::B(a, nn[j], jj, ss[j]) : 0.f;
+      for (int w = 0; w < RA; ++w) {
+        const int jj = j0 + rsub + 32 * w;
+        const int jc = jj < F::J ? jj : F::J - 1;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
-        const int off = swz(row, c);
-        st_shared_v4(sa_hi + off, h[0], h[1], h[2], h[3]);
-        st_shared_v4(sa_lo + off, l[0], l[1], l[2], l[3]);
+        for (int j = 0; j < 4; ++j) {
+          const float v = F::B(a, nn[j], jc, ss[j]);
+          va[w][j] = (okk[j] && jj < F::J) ? v : 0.f;
+        }
       }
-      for (int row = rsub; row < NT; row += 32) {
-        const int mm = m0 + row;
-        float v[4], h[4], l[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = (okk[j] && mm < F::M) ? F::A(a, nn[j], mm, ss[j]) : 0.f;
+      for (int w = 0; w < RB; ++w) {
+        const int mm = m0 + rsub + 32 * w;
+        const int mc = mm < F::M ? mm : F::M - 1;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) split_tf32(v[j], h[j], l[j]);
-        const int off = swz(row, c);
-        st_shared_v4(sb_hi + off, h[0], h[1], h[2], h[3]);
-        st_shared_v4(sb_lo + off, l[0], l[1], l[2], l[3]);
+        for (int j = 0; j < 4; ++j) {
+          const float v = F::A(a, nn[j], mc, ss[j]);
+          vb[w][j] = (okk[j] && mm < F::M && rsub + 32 * w < NT) ? v : 0.f;
+        }
+      }
+    };
+    if (KB > 0) gather(0);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* sa_hi = smem + st * L::STAGE;
+      uint8_t* sa_lo = sa_hi + L::A_BYTES;
+      uint8_t* sb_hi = sa_lo + L::A_BYTES;
+      uint8_t* sb_lo = sb_hi + L::B_BYTES;
+#pragma unroll
+      for (int w = 0; w < RA; ++w) {
+        float h[4], l[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) split_tf32(va[w][j], h[j], l[j]);
+        const int off = swz(rsub + 32 * w, c);
+        *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+#pragma unroll
+      for (int w = 0; w < RB; ++w) {
+        const int row = rsub + 32 * w;
+        if (row < NT) {
+          float h[4], l[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split_tf32(vb[w][j], h[j], l[j]);
+          const int off = swz(row, c);
+          *reinterpret_cast<float4*>(sb_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(sb_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        }
       }
       fence_async_smem();
       mbar_arrive(&full[st]);
+      if (kb + 1 < KB) gather(kb + 1);
     }
     mbar_wait(done, 0);
     fence_after();
@@ -580,7 +674,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
         }
       }
     }
-  } else if (lane == 0) {
+  } else if (warp == kProducerWarps && lane == 0) {
     if (KB > 0) mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
     else tc::mbar_arrive(done);
   }

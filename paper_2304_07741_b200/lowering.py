@@ -51,8 +51,9 @@ POINTWISE_BLOCK = 256
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
 GEMM_TILE = 64
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
-TC_THREADS = 288  # tcgen05 GEMM: 8 producer/epilogue warps + 1 MMA warp
+TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
+TC_SMEM_PAIR = 110 * 1024  # two CTAs per SM when a 2-stage ring fits
 TC_WGRAD_TCHUNK = 4096  # pixels per wgrad split (128 k-blocks of 32)
 
 
@@ -61,6 +62,8 @@ def tc_tile(cols: int) -> tuple[int, int, int]:
     nct = -(-cols // 256)
     nt = -(-(-(-cols // nct)) // 16) * 16
     stage = 2 * 128 * 128 + 2 * nt * 128
+    if 2 * stage + 2048 <= TC_SMEM_PAIR:
+        return nt, nct, 2
     stages = max(2, min(4, TC_SMEM_BUDGET // stage))
     return nt, nct, stages
 
@@ -829,8 +832,22 @@ class Lowerer:
         if self.use_tc and M >= 8 and K >= 16:
             nt, nct, stages = tc_tile(M)
             smem = tc_smem_bytes(nt, stages)
-            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, 1) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}>(a); }}\n'
+            kb = -(-K // 32)
+            pack_bytes = nct * kb * 2 * nt * 128
+            if phase == 0:
+                self.p.saved.append(SizeRule(0, 1, pack_bytes))
+                pslot = self.p.slot_saved(len(self.p.saved) - 1)
+            else:
+                k_ws, _ = self._new_ws((1,))
+                self.p.ws[k_ws] = SizeRule(0, 1, pack_bytes)
+                pslot = -1 - k_ws
+            ploc = fa.ptr(pslot)
+            functor = functor[: functor.rindex("};")] + f"  static __device__ __forceinline__ float* packed(const CanvasArgs& a) {{ return {ploc}; }}\n}};\n"
+            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
+            pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
+            total = nct * kb * nt * 32
+            self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
             grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
             self.p.launches.append(Launch("kernel", phase, name, k, TC_THREADS, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
             return
@@ -841,7 +858,7 @@ class Lowerer:
 
     def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops) -> None:
         """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
-        use_tc = self.use_tc and J >= 32 and M >= 8
+        use_tc = self.use_tc and J >= 32
         tchunk = TC_WGRAD_TCHUNK if use_tc else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
         self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
@@ -866,7 +883,7 @@ class Lowerer:
         if use_tc:
             nt, nct, stages = tc_tile(M)
             smem = tc_smem_bytes(nt, stages)
-            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, 1) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}>(a); }}\n'
+            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             grid = (GridRule(0, J, 128), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
             self.p.launches.append(Launch("kernel", 1, name, k, TC_THREADS, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))

@@ -87,8 +87,10 @@ void reduce_partials(const CanvasArgs& a) {
     a.p[1][idx] = s;
   }
 }
-template <class F, int NT, int STAGES>
+template <class F, int NT, int STAGES, bool PACKED>
 void tc_gemm_pix(const CanvasArgs& a) { gemm_nk<F>(a); }
+template <class F, int NT>
+void tc_pack_b(const CanvasArgs&) {}
 template <class F, int NT, int STAGES>
 void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 }  // namespace canvas
