@@ -68,7 +68,7 @@ def pinned_source() -> str:
         p = plan_for(text, c_in=64, c_out=64, h=56, w=56, k=3, g=4)
         src = p.source.replace('#include "canvas_kernels.cuh"\n', "")
         # kernel names are per-plan; prefix them so one translation unit holds all
-        pat = re.compile(r"\b(" + "|".join(map(re.escape, p.kernel_names)) + r")\b")
+        pat = re.compile(r"\b((?:" + "|".join(map(re.escape, p.kernel_names)) + r")(?:_F)?)\b")
         src = pat.sub(lambda m: f"{name}_{m.group(1)}", src)
         parts.append(f"// ---- {name}\n" + src)
     return '#include "canvas_kernels.cuh"\n' + "\n".join(parts)

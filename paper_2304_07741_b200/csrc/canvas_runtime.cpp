@@ -187,6 +187,7 @@ struct canvas_plan {
   CUcontext ctx = nullptr;
   int64_t n_fc = 0, copies = 1;
   int64_t x_off = 0, y_off = 0, dx_off = 0, dy_off = 0;  // per-copy element offsets
+  int64_t max_batch = 0;  // kernels use 32-bit per-tensor offsets up to this batch
   std::vector<SizeRule> saved, ws;
   std::vector<Record> recs;
   std::vector<CUfunction> fns;
@@ -297,7 +298,8 @@ void* slot_ptr(const canvas_plan* p, int64_t s, int64_t copy, int64_t batch, con
 int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, const float* const* w, int n_fc,
               float* y, const float* dy, float* dx, float* const* dw, void* saved, void* ws, void* stream) {
   if (!p) return fail(CANVAS_ERR_ARGS, "null plan");
-  if (batch < 1) return fail(CANVAS_ERR_ARGS, "batch must be >= 1");
+  if (batch < 1 || batch > p->max_batch)
+    return fail(CANVAS_ERR_ARGS, "batch " + std::to_string(batch) + " outside [1, " + std::to_string(p->max_batch) + "]");
   if (n_fc != p->n_fc * p->copies)
     return fail(CANVAS_ERR_ARGS, "expected " + std::to_string(p->n_fc * p->copies) + " FC weights, got " +
                                      std::to_string(n_fc));
@@ -386,6 +388,7 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
   p->y_off = rd.i64();
   p->dx_off = rd.i64();
   p->dy_off = rd.i64();
+  p->max_batch = rd.i64();
   int64_t src_len = rd.i64(), names_len = rd.i64();
   if (!rd.ok || n_kernels < 0 || n_launch < 0 || n_saved < 0 || n_ws < 0 || p->copies < 1)
     return fail(CANVAS_ERR_BLOB, "bad blob header");

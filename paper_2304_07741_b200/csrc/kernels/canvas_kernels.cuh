@@ -273,9 +273,29 @@ __device__ __forceinline__ cv_u64 desc_k_sw128(cv_u32 saddr) {
   return d;
 }
 
-// instruction descriptor: kind::tf32, D fp32, A/B K-major, M=128, N=n
-__host__ __device__ constexpr cv_u32 idesc_tf32(int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((cv_u32)(n >> 3) << 17) | ((cv_u32)(128 >> 4) << 24);
+// MN-major, 128B-swizzle smem descriptor: 32 consecutive M elements per 128 B
+// row, 8 K rows per 1024 B atom; M blocks of 32 are `lbo` bytes apart.
+__device__ __forceinline__ cv_u64 desc_mn_sw128(cv_u32 saddr, cv_u32 lbo, cv_u32 sbo) {
+  cv_u64 d = 0;
+  d |= (cv_u64)((saddr >> 4) & 0x3FFF);
+  d |= (cv_u64)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (cv_u64)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (cv_u64)1 << 46;
+  d |= (cv_u64)2 << 61;
+  return d;
+}
+
+// instruction descriptor: kind::tf32, D fp32, M=128, N=n; A K-major or MN-major, B K-major
+__host__ __device__ constexpr cv_u32 idesc_tf32(int n, bool a_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((cv_u32)(n >> 3) << 17) |
+         ((cv_u32)(128 >> 4) << 24);
+}
+
+// byte offset of element (m, k) of a 128 x 32 MN-major SW128 tile laid out as
+// [k-group (4)][m-block (4)] atoms of 1024 B (LBO = 1024, SBO = 4096)
+__device__ __forceinline__ int mn_off(int m, int k) {
+  const int j = k & 7;
+  return (((k >> 3) * 4 + (m >> 5)) << 10) + j * 128 + ((((m >> 2) & 7) ^ j) << 4) + (m & 3) * 4;
 }
 
 __device__ __forceinline__ void mma_tf32(cv_u32 dtmem, cv_u64 adesc, cv_u64 bdesc, cv_u32 idesc, cv_u32 accum) {
@@ -338,10 +358,10 @@ struct Smem {
 };
 
 // MMA issuer: consumes STAGES-deep ring, 3 MMAs per K=8 step (hi.hi, hi.lo, lo.hi)
-template <int NT, int STAGES>
+template <int NT, int STAGES, bool A_MN = false>
 __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* empty, cv_u64* done, cv_u32 tmem, int KB) {
   using L = Smem<NT, STAGES>;
-  constexpr cv_u32 idesc = idesc_tf32(NT);
+  constexpr cv_u32 idesc = idesc_tf32(NT, A_MN);
   for (int kb = 0; kb < KB; ++kb) {
     const int st = kb % STAGES;
     mbar_wait(&full[st], (kb / STAGES) & 1);
@@ -353,9 +373,17 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
 #pragma unroll
     for (int kk = 0; kk < kBK / 8; ++kk) {
       const cv_u32 o = kk * 32;  // 8 tf32 = 32 B along K inside the swizzled row
-      mma_tf32(tmem, desc_k_sw128(a_hi + o), desc_k_sw128(b_hi + o), idesc, (kb | kk) != 0);
-      mma_tf32(tmem, desc_k_sw128(a_hi + o), desc_k_sw128(b_lo + o), idesc, 1);
-      mma_tf32(tmem, desc_k_sw128(a_lo + o), desc_k_sw128(b_hi + o), idesc, 1);
+      cv_u64 dah, dal;
+      if (A_MN) {
+        dah = desc_mn_sw128(a_hi + kk * 4096, 1024, 4096);
+        dal = desc_mn_sw128(a_lo + kk * 4096, 1024, 4096);
+      } else {
+        dah = desc_k_sw128(a_hi + o);
+        dal = desc_k_sw128(a_lo + o);
+      }
+      mma_tf32(tmem, dah, desc_k_sw128(b_hi + o), idesc, (kb | kk) != 0);
+      mma_tf32(tmem, dah, desc_k_sw128(b_lo + o), idesc, 1);
+      mma_tf32(tmem, dal, desc_k_sw128(b_hi + o), idesc, 1);
     }
     commit(&empty[st]);
   }
@@ -402,7 +430,52 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   const int c0 = blockIdx.y * NT;
 
   if (warp < kProducerWarps) {
-    const int p = threadIdx.x;          // 0..255
+    const int p = threadIdx.x;  // 0..255
+    if (PACKED) {
+      // MN-major A: thread = one k of the 32-wide k-block (kr) x 16 pixels
+      // (4 blocks of 4 consecutive); the functor's k-dependent index math is
+      // shared by its 16 evaluations.
+      const int kr = p >> 3, c = p & 7;
+      int pn[16], ps[16];
+      unsigned okmask = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const long long t = t0 + (i >> 2) * 32 + c * 4 + (i & 3);
+        okmask |= (t < T ? 1u : 0u) << i;
+        const long long tc = t < T ? t : T - 1;
+        pn[i] = (int)(tc / F::S);
+        ps[i] = (int)(tc - (long long)pn[i] * F::S);
+      }
+      float va[16];
+      auto gather = [&](int kb) {
+        const int k = kb * kBK + kr;
+        const int kc = k < F::K ? k : F::K - 1;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float v = F::B(a, (long long)pn[i], kc, ps[i]);
+          va[i] = (((okmask >> i) & 1u) && k < F::K) ? v : 0.f;
+        }
+      };
+      gather(0);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+        uint8_t* sa_hi = smem + st * L::STAGE;
+        uint8_t* sa_lo = sa_hi + L::A_BYTES;
+#pragma unroll
+        for (int mb = 0; mb < 4; ++mb) {
+          float h[4], l[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) split_tf32(va[mb * 4 + j], h[j], l[j]);
+          const int off = mn_off(mb * 32 + c * 4, kr);
+          *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+        fence_async_smem();
+        mbar_arrive(&full[st]);
+        if (kb + 1 < KB) gather(kb + 1);
+      }
+    } else {
     const int r = p & (kBM - 1);        // tile row (pixel)
     const int half = p >> 7;            // 16 k of the 32-wide k-block
     const long long t = t0 + r;
@@ -471,6 +544,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       mbar_arrive(&full[st]);
       if (kb + 1 < KB) gather(kb + 1);
     }
+    }
     // epilogue: TMEM lane quadrant = warp % 4, column half = warp / 4
     mbar_wait(done, 0);
     fence_after();
@@ -494,7 +568,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       }
     }
   } else if (warp == kProducerWarps) {
-    if (lane == 0) mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
+    if (lane == 0) mma_loop<NT, STAGES, PACKED>(smem, full, empty, done, tmem, KB);
   } else if (PACKED && lane == 0) {
     // B operand: pre-split, pre-swizzled weight tile images (tc_pack_b), one
     // TMA bulk copy of {hi, lo} per k-block

@@ -32,6 +32,7 @@ max-subtracted (A.7); FC dense, bias-free, W[out, prod(in ch)] (A.4).
 from __future__ import annotations
 
 import math
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -50,10 +51,11 @@ BETA_NONE, BETA_AFTER_FIRST, BETA_ALWAYS = 0, 1, 2
 POINTWISE_BLOCK = 256
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
 GEMM_TILE = 64
+MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
 TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
-TC_SMEM_PAIR = 110 * 1024  # two CTAs per SM when a 2-stage ring fits
+TC_SMEM_PAIR = 110 * 1024 if os.environ.get("CANVAS_TC_PAIR", "1") == "1" else 0  # two CTAs/SM when a 2-stage ring fits
 TC_WGRAD_TCHUNK = 4096  # pixels per wgrad split (128 k-blocks of 32)
 
 
@@ -172,7 +174,7 @@ class Plan:
 
         header: magic[8], then int64s: version, n_kernels, n_launches, n_saved,
         n_ws, n_fc, copies, x_copy_off, y_copy_off, dx_copy_off, dy_copy_off,
-        src_len, names_len; then (a_num, a_den, b) per saved and per ws slot;
+        max_batch, src_len, names_len; then (a_num, a_den, b) per saved and per ws slot;
         then per launch: kind, phase, kernel, block, smem, 3x(a,b,d,cap), nslots,
         slots[MAX_KSLOTS], beta, memset_slot, memset (a_num,a_den,b); then the
         CUDA source and the NUL-separated kernel names.
@@ -181,7 +183,7 @@ class Plan:
         src = self.source.encode()
         q = struct.Struct("<q")
         out = bytearray(BLOB_MAGIC)
-        hdr = [ABI_VERSION, len(self.kernel_names), len(self.launches), len(self.saved), len(self.ws), self.n_fc, self.copies, self.x_copy_off, self.y_copy_off, self.dx_copy_off, self.dy_copy_off, len(src), len(names)]
+        hdr = [ABI_VERSION, len(self.kernel_names), len(self.launches), len(self.saved), len(self.ws), self.n_fc, self.copies, self.x_copy_off, self.y_copy_off, self.dx_copy_off, self.dy_copy_off, MAX_BATCH, len(src), len(names)]
         for v in hdr:
             out += q.pack(v)
         for r in self.saved + self.ws:
@@ -243,6 +245,7 @@ class Fn:
         self.k = 0
         self.local_slots: list[int] = []
         self.bases: dict = {}
+        self.flat_of: dict = {}  # coordinate tuple -> (flat index var, extents)
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -300,32 +303,57 @@ class Fn:
             self.local_slots.append(slot)
         return f"a.p[{self.local_slots.index(slot)}]"
 
-    def base(self, d: TDesc) -> str:
-        """Per-image base pointer of a tensor (``n`` is the image index)."""
+    def base(self, d: TDesc) -> tuple[str, str]:
+        """(pointer, per-image element offset) of a tensor (``n`` = image index).
+
+        Tensors whose MAX_BATCH images fit in 2^31 elements use 32-bit offset
+        arithmetic (one IMAD per access); larger ones a 64-bit image base."""
         key = (d.slot, d.bstride)
         if key in self.bases:
             return self.bases[key]
         b = self.fresh("b")
-        self.bases[key] = b
         # hoisted: emitted into the preamble (before any scope) by the caller
-        self.pre.append(f"float* __restrict__ {b} = {self.ptr(d.slot)} + n * {d.bstride}LL;")
-        return b
+        if d.bstride * MAX_BATCH < 2**31:
+            self.pre.append(f"const int {b} = (int)n * {d.bstride};")
+            r = (self.ptr(d.slot), b)
+        else:
+            self.pre.append(f"float* __restrict__ {b} = {self.ptr(d.slot)} + n * {d.bstride}LL;")
+            r = (b, "")
+        self.bases[key] = r
+        return r
 
     def offset(self, d: TDesc, coords) -> str:
-        terms = [f"{c}*{s}" if s != 1 else f"{c}" for c, s in zip(coords, d.strides) if s != 0 and c != "0"]
+        coords, strides = list(coords), list(d.strides)
+        # a suffix of coordinates that is the decomposition of a flat index over
+        # contiguous dims collapses back to that index (e.g. (h, w) -> s)
+        for L in range(len(coords), 1, -1):
+            got = self.flat_of.get(tuple(coords[-L:]))
+            if got is None:
+                continue
+            flat, ext = got
+            st = strides[-L:]
+            contig = all(st[i] == st[i + 1] * ext[i + 1] for i in range(L - 1))
+            if tuple(ext) == tuple(d.dims[-L:]) and contig:
+                coords = coords[:-L] + [flat]
+                strides = strides[:-L] + [st[-1]]
+                break
+        terms = [f"{c}*{s}" if s != 1 else f"{c}" for c, s in zip(coords, strides) if s != 0 and c != "0"]
         return self.ivar(" + ".join(terms) if terms else "0")
 
-    def load(self, d: TDesc, coords) -> str:
+    def addr(self, d: TDesc, coords) -> str:
         off = self.offset(d, coords)
-        return self.fvar(f"__ldg({self.base(d)} + {off})")
+        p, nb = self.base(d)
+        return f"{p} + ({nb} + {off})" if nb else f"{p} + {off}"
+
+    def load(self, d: TDesc, coords) -> str:
+        return self.fvar(f"__ldg({self.addr(d, coords)})")
 
     def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
-        off = self.offset(d, coords)
-        b = self.base(d)
+        a = self.addr(d, coords)
         if beta:
-            self.emit(f"if (a.beta) {b}[{off}] += {val}; else {b}[{off}] = {val};")
+            self.emit(f"if (a.beta) *({a}) += {val}; else *({a}) = {val};")
         else:
-            self.emit(f"{b}[{off}] = {val};")
+            self.emit(f"*({a}) = {val};")
 
     def decompose(self, flat: str, ext) -> list[str]:
         """Row-major flat index -> coordinates (constant divisors)."""
@@ -340,6 +368,8 @@ class Fn:
             else:
                 coords[i] = self.ivar(f"{rest} % {e}")
                 rest = self.ivar(f"{rest} / {e}")
+        if len(ext) > 1:
+            self.flat_of.setdefault(tuple(coords), (flat, tuple(ext)))
         return coords
 
     def flatten(self, coords, ext) -> str:
