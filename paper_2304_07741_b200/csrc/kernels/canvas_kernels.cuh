@@ -273,15 +273,17 @@ __device__ __forceinline__ cv_u64 desc_k_sw128(cv_u32 saddr) {
   return d;
 }
 
-// MN-major, 128B-swizzle smem descriptor: 32 consecutive M elements per 128 B
-// row, 8 K rows per 1024 B atom; M blocks of 32 are `lbo` bytes apart.
-__device__ __forceinline__ cv_u64 desc_mn_sw128(cv_u32 saddr, cv_u32 lbo, cv_u32 sbo) {
+// MN-major smem descriptor for 32-bit (tf32) operands: the only legal MN-major
+// tf32 layout is SWIZZLE_128B_BASE32B — 128 B rows of 32 consecutive M
+// elements, 4 K rows per 512 B atom, 32 B chunks XOR-permuted by row; M blocks
+// of 32 are `lbo` bytes apart, K groups of 4 rows `sbo` bytes apart.
+__device__ __forceinline__ cv_u64 desc_mn_sw128_32b(cv_u32 saddr, cv_u32 lbo, cv_u32 sbo) {
   cv_u64 d = 0;
   d |= (cv_u64)((saddr >> 4) & 0x3FFF);
   d |= (cv_u64)((lbo >> 4) & 0x3FFF) << 16;
   d |= (cv_u64)((sbo >> 4) & 0x3FFF) << 32;
   d |= (cv_u64)1 << 46;
-  d |= (cv_u64)2 << 61;
+  d |= (cv_u64)1 << 61;  // SWIZZLE_128B_BASE32B
   return d;
 }
 
@@ -291,11 +293,12 @@ __host__ __device__ constexpr cv_u32 idesc_tf32(int n, bool a_mn = false) {
          ((cv_u32)(128 >> 4) << 24);
 }
 
-// byte offset of element (m, k) of a 128 x 32 MN-major SW128 tile laid out as
-// [k-group (4)][m-block (4)] atoms of 1024 B (LBO = 1024, SBO = 4096)
+// byte offset of element (m, k) of a 128 x 32 MN-major SW128_BASE32B tile laid
+// out as [k-group of 4 rows (8)][m-block of 32 (4)] atoms of 512 B
+// (LBO = 512, SBO = 2048; one K=8 MMA spans two k-groups = 4096 B)
 __device__ __forceinline__ int mn_off(int m, int k) {
-  const int j = k & 7;
-  return (((k >> 3) * 4 + (m >> 5)) << 10) + j * 128 + ((((m >> 2) & 7) ^ j) << 4) + (m & 3) * 4;
+  const int j = k & 3;
+  return (((k >> 2) * 4 + (m >> 5)) << 9) + j * 128 + ((((m >> 3) & 3) ^ j) << 5) + (m & 7) * 4;
 }
 
 __device__ __forceinline__ void mma_tf32(cv_u32 dtmem, cv_u64 adesc, cv_u64 bdesc, cv_u32 idesc, cv_u32 accum) {
@@ -375,8 +378,8 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
       const cv_u32 o = kk * 32;  // 8 tf32 = 32 B along K inside the swizzled row
       cv_u64 dah, dal;
       if (A_MN) {
-        dah = desc_mn_sw128(a_hi + kk * 4096, 1024, 4096);
-        dal = desc_mn_sw128(a_lo + kk * 4096, 1024, 4096);
+        dah = desc_mn_sw128_32b(a_hi + kk * 4096, 512, 2048);
+        dal = desc_mn_sw128_32b(a_lo + kk * 4096, 512, 2048);
       } else {
         dah = desc_k_sw128(a_hi + o);
         dal = desc_k_sw128(a_lo + o);
@@ -397,7 +400,7 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
 // MMA rows = 128 pixels t = n*S + s (operand B(n,k,s), computed), MMA cols =
 // NT output channels (operand A(m,k), weights).
 // ---------------------------------------------------------------------------
-template <class F, int NT, int STAGES, bool PACKED>
+template <class F, int NT, int STAGES, bool PACKED, bool A_MN>
 __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   using namespace tc;
   using L = Smem<NT, STAGES>;
@@ -431,29 +434,32 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
 
   if (warp < kProducerWarps) {
     const int p = threadIdx.x;  // 0..255
-    if (PACKED) {
-      // MN-major A: thread = one k of the 32-wide k-block (kr) x 16 pixels
-      // (4 blocks of 4 consecutive); the functor's k-dependent index math is
-      // shared by its 16 evaluations.
-      const int kr = p >> 3, c = p & 7;
-      int pn[16], ps[16];
+    if (A_MN) {
+      // MN-major A: warp w owns k-rows 4w..4w+3 of the 32-wide k-block, lane =
+      // pixel within each 32-pixel block (4 blocks).  k is warp-uniform, so the
+      // functor's channel index math runs once per k on the uniform datapath;
+      // loads are 128 B coalesced; smem stores hit one 128 B swizzled row.
+      int pn[4], ps[4];
       unsigned okmask = 0;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const long long t = t0 + (i >> 2) * 32 + c * 4 + (i & 3);
-        okmask |= (t < T ? 1u : 0u) << i;
+      for (int mb = 0; mb < 4; ++mb) {
+        const long long t = t0 + mb * 32 + lane;
+        okmask |= (t < T ? 1u : 0u) << mb;
         const long long tc = t < T ? t : T - 1;
-        pn[i] = (int)(tc / F::S);
-        ps[i] = (int)(tc - (long long)pn[i] * F::S);
+        pn[mb] = (int)(tc / F::S);
+        ps[mb] = (int)(tc - (long long)pn[mb] * F::S);
       }
-      float va[16];
+      float va[4][4];
       auto gather = [&](int kb) {
-        const int k = kb * kBK + kr;
-        const int kc = k < F::K ? k : F::K - 1;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float v = F::B(a, (long long)pn[i], kc, ps[i]);
-          va[i] = (((okmask >> i) & 1u) && k < F::K) ? v : 0.f;
+        for (int q = 0; q < 4; ++q) {
+          const int k = kb * kBK + warp * 4 + q;
+          const int kc = k < F::K ? k : F::K - 1;
+#pragma unroll
+          for (int mb = 0; mb < 4; ++mb) {
+            const float v = F::B(a, (long long)pn[mb], kc, ps[mb]);
+            va[q][mb] = (((okmask >> mb) & 1u) && k < F::K) ? v : 0.f;
+          }
         }
       };
       gather(0);
@@ -463,14 +469,15 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         uint8_t* sa_hi = smem + st * L::STAGE;
         uint8_t* sa_lo = sa_hi + L::A_BYTES;
 #pragma unroll
-        for (int mb = 0; mb < 4; ++mb) {
-          float h[4], l[4];
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) split_tf32(va[mb * 4 + j], h[j], l[j]);
-          const int off = mn_off(mb * 32 + c * 4, kr);
-          *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
-        }
+          for (int mb = 0; mb < 4; ++mb) {
+            float h, l;
+            split_tf32(va[q][mb], h, l);
+            const int off = mn_off(mb * 32 + lane, warp * 4 + q);
+            *reinterpret_cast<float*>(sa_hi + off) = h;
+            *reinterpret_cast<float*>(sa_lo + off) = l;
+          }
         fence_async_smem();
         mbar_arrive(&full[st]);
         if (kb + 1 < KB) gather(kb + 1);
@@ -568,7 +575,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       }
     }
   } else if (warp == kProducerWarps) {
-    if (lane == 0) mma_loop<NT, STAGES, PACKED>(smem, full, empty, done, tmem, KB);
+    if (lane == 0) mma_loop<NT, STAGES, A_MN>(smem, full, empty, done, tmem, KB);
   } else if (PACKED && lane == 0) {
     // B operand: pre-split, pre-swizzled weight tile images (tc_pack_b), one
     // TMA bulk copy of {hi, lo} per k-block

@@ -56,6 +56,7 @@ SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4
 TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
 TC_SMEM_PAIR = 110 * 1024 if os.environ.get("CANVAS_TC_PAIR", "1") == "1" else 0  # two CTAs/SM when a 2-stage ring fits
+TC_A_MN = "true" if os.environ.get("CANVAS_TC_AMN", "1") == "1" else "false"  # computed operand layout
 TC_WGRAD_TCHUNK = 4096  # pixels per wgrad split (128 k-blocks of 32)
 
 
@@ -873,7 +874,7 @@ class Lowerer:
                 pslot = -1 - k_ws
             ploc = fa.ptr(pslot)
             functor = functor[: functor.rindex("};")] + f"  static __device__ __forceinline__ float* packed(const CanvasArgs& a) {{ return {ploc}; }}\n}};\n"
-            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true>(a); }}\n'
+            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true, {TC_A_MN}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
             total = nct * kb * nt * 32
