@@ -247,6 +247,7 @@ class Fn:
         self.local_slots: list[int] = []
         self.bases: dict = {}
         self.flat_of: dict = {}  # coordinate tuple -> (flat index var, extents)
+        self.raw: set = set()  # coordinate vars that may be out of range (Shift/Unfold sources)
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -346,7 +347,14 @@ class Fn:
         p, nb = self.base(d)
         return f"{p} + ({nb} + {off})" if nb else f"{p} + {off}"
 
-    def load(self, d: TDesc, coords) -> str:
+    def raw_ivar(self, expr: str) -> str:
+        v = self.ivar(expr)
+        self.raw.add(v)
+        return v
+
+    def load(self, d: TDesc, coords, preds: tuple = ()) -> str:
+        if preds:
+            return self.fvar(f"({' && '.join(preds)}) ? __ldg({self.addr(d, coords)}) : 0.f")
         return self.fvar(f"__ldg({self.addr(d, coords)})")
 
     def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
@@ -439,44 +447,56 @@ class Lowerer:
         return TDesc(slot, ctot * h * w, (h * w, w, 1), (c, h, w))
 
     # -------------------------------------------------------------- forward values
-    def val(self, f: Fn, v: int, coords: tuple) -> str:
-        key = ("val", v, coords)
+    def val(self, f: Fn, v: int, coords: tuple, preds: tuple = ()) -> str:
+        """Forward value of node v at ``coords``.  ``preds`` are the in-range
+        predicates of the Shift/Unfold stages between the requesting load and v
+        (App. A.3: every stage applies its own); they fold into a predicated
+        load at a materialised tensor, or a select around a computed node."""
+        key = ("val", v, coords, preds)
         got = f.memo_get(key)
         if got:
             return got
+        nd = self.nodes[v]
         if v in self.fwd_desc and v != getattr(f, "computing", None):
-            r = f.load(self.fwd_desc[v], coords)
+            r = f.load(self.fwd_desc[v], coords, preds)
+        elif nd.op in VIEW_OPS:
+            r = self.view(f, v, coords, preds)
+        elif preds:
+            cc = tuple(f.ivar(f"min(max({c}, 0), {nd.ext[i] - 1})") if c in f.raw else c for i, c in enumerate(coords))
+            inner = self.compute(f, v, cc)
+            r = f.fvar(f"({' && '.join(preds)}) ? {inner} : 0.f")
         else:
             r = self.compute(f, v, coords)
         f.memo_put(key, r)
         return r
 
-    def compute(self, f: Fn, v: int, coords: tuple) -> str:
+    def view(self, f: Fn, v: int, coords: tuple, preds: tuple) -> str:
         nd = self.nodes[v]
         op, at = nd.op, nd.attr
         if op == "group":
             d, b = at["dim"], at["B"]
             merged = f.ivar(f"{coords[d]}*{b} + {coords[d + 1]}" if coords[d] != "0" else coords[d + 1])
-            return self.val(f, nd.ins[0], coords[:d] + (merged,) + coords[d + 2 :])
+            return self.val(f, nd.ins[0], coords[:d] + (merged,) + coords[d + 2 :], preds)
         if op == "shift":
             ax, off = at["ax"], at["off"]
             e = nd.ext[ax]
-            src = f.ivar(f"{coords[ax]} + ({off})")
-            pred = f"((unsigned){src} < {e}u)"
-            cl = f.ivar(f"min(max({src}, 0), {e - 1})")
-            inner = self.val(f, nd.ins[0], coords[:ax] + (cl,) + coords[ax + 1 :])
-            return f.fvar(f"{pred} ? {inner} : 0.f")
+            src = f.raw_ivar(f"{coords[ax]} + ({off})")
+            return self.val(f, nd.ins[0], coords[:ax] + (src,) + coords[ax + 1 :], preds + (f"((unsigned){src} < {e}u)",))
         if op == "unfold":
             k_at, K, ax_out = at["at"], at["K"], at["ax_out"]
             e = nd.ext[ax_out]
-            src = f.ivar(f"{coords[ax_out]} + {coords[k_at]} - {K // 2}")
-            pred = f"((unsigned){src} < {e}u)"
-            cl = f.ivar(f"min(max({src}, 0), {e - 1})")
+            src = f.raw_ivar(f"{coords[ax_out]} + {coords[k_at]} - {K // 2}")
             c2 = list(coords)
-            c2[ax_out] = cl
+            c2[ax_out] = src
             del c2[k_at]
-            inner = self.val(f, nd.ins[0], tuple(c2))
-            return f.fvar(f"{pred} ? {inner} : 0.f")
+            return self.val(f, nd.ins[0], tuple(c2), preds + (f"((unsigned){src} < {e}u)",))
+        raise LoweringError(op)
+
+    def compute(self, f: Fn, v: int, coords: tuple) -> str:
+        nd = self.nodes[v]
+        op, at = nd.op, nd.attr
+        if op in VIEW_OPS:
+            return self.view(f, v, coords, ())
         if op == "ew":
             x = self.val(f, nd.ins[0], coords)
             return f.fvar(_EW_FWD[at["fn"]].format(x))
@@ -501,15 +521,20 @@ class Lowerer:
         return coords[:cs] + lc + coords[cs + nr :]
 
     # -------------------------------------------------------------- gradients
-    def grad(self, f: Fn, v: int, coords: tuple) -> str:
-        key = ("grad", v, coords)
+    def grad(self, f: Fn, v: int, coords: tuple, preds: tuple = ()) -> str:
+        key = ("grad", v, coords, preds)
         got = f.memo_get(key)
         if got:
             return got
         if v == self.out:
-            r = f.load(self.dy_desc, coords)
+            r = f.load(self.dy_desc, coords, preds)
         elif v in self.grad_desc and v != self.computing_grad:
-            r = f.load(self.grad_desc[v], coords)
+            r = f.load(self.grad_desc[v], coords, preds)
+        elif preds:
+            nd = self.nodes[v]
+            cc = tuple(f.ivar(f"min(max({c}, 0), {nd.ext[i] - 1})") if c in f.raw else c for i, c in enumerate(coords))
+            g = self.grad_sum(f, v, cc)
+            r = f.fvar(f"({' && '.join(preds)}) ? {g} : 0.f")
         else:
             r = self.grad_sum(f, v, coords)
         f.memo_put(key, r)
@@ -534,23 +559,19 @@ class Lowerer:
         if op == "shift":
             ax, off = at["ax"], at["off"]
             e = nu.ext[ax]
-            src = f.ivar(f"{coords[ax]} - ({off})")
-            cl = f.ivar(f"min(max({src}, 0), {e - 1})")
-            g = self.grad(f, u, coords[:ax] + (cl,) + coords[ax + 1 :])
-            return f.fvar(f"((unsigned){src} < {e}u) ? {g} : 0.f")
+            src = f.raw_ivar(f"{coords[ax]} - ({off})")
+            return self.grad(f, u, coords[:ax] + (src,) + coords[ax + 1 :], (f"((unsigned){src} < {e}u)",))
         if op == "unfold":
             # col2im as a gather: dI[h] = sum_k dU[k, h - k + K//2] (valid terms only)
             k_at, K, ax_in = at["at"], at["K"], at["ax_in"]
             e = nu.ext[at["ax_out"]]
             terms = []
             for k in range(K):
-                src = f.ivar(f"{coords[ax_in]} - ({k - K // 2})")
-                cl = f.ivar(f"min(max({src}, 0), {e - 1})")
+                src = f.raw_ivar(f"{coords[ax_in]} - ({k - K // 2})")
                 c2 = list(coords)
-                c2[ax_in] = cl
+                c2[ax_in] = src
                 c2.insert(k_at, str(k))
-                g = self.grad(f, u, tuple(c2))
-                terms.append(f"(((unsigned){src} < {e}u) ? {g} : 0.f)")
+                terms.append(self.grad(f, u, tuple(c2), (f"((unsigned){src} < {e}u)",)))
             return f.fvar(" + ".join(terms))
         if op == "ew":
             g = self.grad(f, u, coords)
