@@ -248,6 +248,11 @@ class Fn:
         self.bases: dict = {}
         self.flat_of: dict = {}  # coordinate tuple -> (flat index var, extents)
         self.raw: set = set()  # coordinate vars that may be out of range (Shift/Unfold sources)
+        self.lin_of: dict = {}  # affine coordinate var -> ((var, coef)...), const
+        # in-range predicates every load must also satisfy: set while evaluating a
+        # computed node at raw (possibly out-of-range) coordinates whose value is
+        # selected away when the predicates fail (no clamps, no OOB access)
+        self.guard: tuple = ()
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -352,7 +357,46 @@ class Fn:
         self.raw.add(v)
         return v
 
+    def lin(self, x: str) -> tuple[dict, int]:
+        """Affine form {var: coef}, const of a coordinate (var, int literal or affine var)."""
+        x = str(x)
+        if x.lstrip("-").isdigit():
+            return {}, int(x)
+        if x in self.lin_of:
+            terms, c = self.lin_of[x]
+            return dict(terms), c
+        return {x: 1}, 0
+
+    def affine(self, parts, const: int = 0) -> tuple[str, bool]:
+        """Canonical var for sum(coef * part) + const, composing affine coordinates
+        (so e.g. (h - k + 1) + k - 1 folds back to h).  Returns (var, raw): raw is
+        False when the result is a plain in-range coordinate (no predicate needed)."""
+        acc: dict = {}
+        c0 = const
+        for coef, x in parts:
+            t, c = self.lin(x)
+            c0 += coef * c
+            for v, k in t.items():
+                acc[v] = acc.get(v, 0) + coef * k
+        acc = {v: k for v, k in acc.items() if k}
+        if not acc:
+            return str(c0), True
+        if c0 == 0 and len(acc) == 1 and next(iter(acc.values())) == 1:
+            v = next(iter(acc))
+            return v, v in self.raw
+        expr = " + ".join(f"{v}" if k == 1 else f"{v}*({k})" for v, k in sorted(acc.items()))
+        expr = f"{expr} + ({c0})" if c0 else expr
+        v = self.ivar(expr)
+        self.lin_of[v] = (tuple(sorted(acc.items())), c0)
+        self.raw.add(v)
+        return v, True
+
     def load(self, d: TDesc, coords, preds: tuple = ()) -> str:
+        # the guard only protects addresses built from raw (possibly out-of-range)
+        # coordinates; an all-in-range load is safe and stays unpredicated so the
+        # compiler can share it
+        if any(str(c) in self.raw for c in coords):
+            preds = self.guard + tuple(p for p in preds if p not in self.guard)
         if preds:
             return self.fvar(f"({' && '.join(preds)}) ? __ldg({self.addr(d, coords)}) : 0.f")
         return self.fvar(f"__ldg({self.addr(d, coords)})")
@@ -452,7 +496,7 @@ class Lowerer:
         predicates of the Shift/Unfold stages between the requesting load and v
         (App. A.3: every stage applies its own); they fold into a predicated
         load at a materialised tensor, or a select around a computed node."""
-        key = ("val", v, coords, preds)
+        key = ("val", v, coords, preds, f.guard)
         got = f.memo_get(key)
         if got:
             return got
@@ -462,13 +506,21 @@ class Lowerer:
         elif nd.op in VIEW_OPS:
             r = self.view(f, v, coords, preds)
         elif preds:
-            cc = tuple(f.ivar(f"min(max({c}, 0), {nd.ext[i] - 1})") if c in f.raw else c for i, c in enumerate(coords))
-            inner = self.compute(f, v, cc)
+            inner = self.guarded(f, preds, lambda: self.compute(f, v, coords))
             r = f.fvar(f"({' && '.join(preds)}) ? {inner} : 0.f")
         else:
             r = self.compute(f, v, coords)
         f.memo_put(key, r)
         return r
+
+    @staticmethod
+    def guarded(f: Fn, preds: tuple, fn):
+        old = f.guard
+        f.guard = old + tuple(p for p in preds if p not in old)
+        try:
+            return fn()
+        finally:
+            f.guard = old
 
     def view(self, f: Fn, v: int, coords: tuple, preds: tuple) -> str:
         nd = self.nodes[v]
@@ -480,16 +532,18 @@ class Lowerer:
         if op == "shift":
             ax, off = at["ax"], at["off"]
             e = nd.ext[ax]
-            src = f.raw_ivar(f"{coords[ax]} + ({off})")
-            return self.val(f, nd.ins[0], coords[:ax] + (src,) + coords[ax + 1 :], preds + (f"((unsigned){src} < {e}u)",))
+            src, raw = f.affine([(1, coords[ax])], off)
+            pr = preds + (f"((unsigned){src} < {e}u)",) if raw else preds
+            return self.val(f, nd.ins[0], coords[:ax] + (src,) + coords[ax + 1 :], pr)
         if op == "unfold":
             k_at, K, ax_out = at["at"], at["K"], at["ax_out"]
             e = nd.ext[ax_out]
-            src = f.raw_ivar(f"{coords[ax_out]} + {coords[k_at]} - {K // 2}")
+            src, raw = f.affine([(1, coords[ax_out]), (1, coords[k_at])], -(K // 2))
             c2 = list(coords)
             c2[ax_out] = src
             del c2[k_at]
-            return self.val(f, nd.ins[0], tuple(c2), preds + (f"((unsigned){src} < {e}u)",))
+            pr = preds + (f"((unsigned){src} < {e}u)",) if raw else preds
+            return self.val(f, nd.ins[0], tuple(c2), pr)
         raise LoweringError(op)
 
     def compute(self, f: Fn, v: int, coords: tuple) -> str:
@@ -522,7 +576,7 @@ class Lowerer:
 
     # -------------------------------------------------------------- gradients
     def grad(self, f: Fn, v: int, coords: tuple, preds: tuple = ()) -> str:
-        key = ("grad", v, coords, preds)
+        key = ("grad", v, coords, preds, f.guard)
         got = f.memo_get(key)
         if got:
             return got
@@ -531,9 +585,7 @@ class Lowerer:
         elif v in self.grad_desc and v != self.computing_grad:
             r = f.load(self.grad_desc[v], coords, preds)
         elif preds:
-            nd = self.nodes[v]
-            cc = tuple(f.ivar(f"min(max({c}, 0), {nd.ext[i] - 1})") if c in f.raw else c for i, c in enumerate(coords))
-            g = self.grad_sum(f, v, cc)
+            g = self.guarded(f, preds, lambda: self.grad_sum(f, v, coords))
             r = f.fvar(f"({' && '.join(preds)}) ? {g} : 0.f")
         else:
             r = self.grad_sum(f, v, coords)
@@ -559,19 +611,19 @@ class Lowerer:
         if op == "shift":
             ax, off = at["ax"], at["off"]
             e = nu.ext[ax]
-            src = f.raw_ivar(f"{coords[ax]} - ({off})")
-            return self.grad(f, u, coords[:ax] + (src,) + coords[ax + 1 :], (f"((unsigned){src} < {e}u)",))
+            src, raw = f.affine([(1, coords[ax])], -off)
+            return self.grad(f, u, coords[:ax] + (src,) + coords[ax + 1 :], (f"((unsigned){src} < {e}u)",) if raw else ())
         if op == "unfold":
             # col2im as a gather: dI[h] = sum_k dU[k, h - k + K//2] (valid terms only)
             k_at, K, ax_in = at["at"], at["K"], at["ax_in"]
             e = nu.ext[at["ax_out"]]
             terms = []
             for k in range(K):
-                src = f.raw_ivar(f"{coords[ax_in]} - ({k - K // 2})")
+                src, raw = f.affine([(1, coords[ax_in])], -(k - K // 2))
                 c2 = list(coords)
                 c2[ax_in] = src
                 c2.insert(k_at, str(k))
-                terms.append(self.grad(f, u, tuple(c2), (f"((unsigned){src} < {e}u)",)))
+                terms.append(self.grad(f, u, tuple(c2), (f"((unsigned){src} < {e}u)",) if raw else ()))
             return f.fvar(" + ".join(terms))
         if op == "ew":
             g = self.grad(f, u, coords)
