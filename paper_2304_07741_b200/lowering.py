@@ -52,6 +52,7 @@ POINTWISE_BLOCK = 256
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
 GEMM_TILE = 64
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
+REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
 TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
@@ -444,6 +445,7 @@ class Lowerer:
         self.kernels: list[str] = []  # functor + kernel source per kernel
         # forward materialisation: reductions, contractions, input, output (module docstring)
         self.fwd_mat = {0} | {v.id for v in self.nodes if v.op in ("fold", "softmax", "fc")} | {self.out}
+        self.fwd_mat |= self.replicated_pointwise()
         # gradients materialised in the backward: every non-view node except the
         # output (its gradient is dy) — views pull through gathers
         self.grad_mat = {0} | {v.id for v in self.nodes if v.op not in VIEW_OPS and v.id != self.out and v.op != "input"}
@@ -453,6 +455,49 @@ class Lowerer:
         self.dgrad_desc: dict[int, TDesc] = {}  # FC node u -> contribution buffer for its input
         self.dot_desc: dict[int, TDesc] = {}  # softmax node u -> row dot buffer
         self.computing_grad = None
+
+    # -------------------------------------------------------------- materialisation
+    def replicated_pointwise(self) -> set:
+        """Pointwise nodes worth one extra HBM round trip: those whose inline
+        evaluation would be repeated >= REPLICATE_MIN times per consumer output
+        (LHS of a broadcast with ratio M, input of an Unfold, a softmax's three
+        passes, a small FC's per-output-channel dot) and that cost >= 2 loads to
+        recompute.  Walk consumers first so replication compounds through chains."""
+        chosen: set = set()
+        evals: dict = {}
+
+        def mat(v):
+            return v in self.fwd_mat or v in chosen
+
+        def factor(u, pos):
+            nu = self.nodes[u]
+            if nu.op == "bcast":
+                return nu.attr["M"] if pos == 0 else 1
+            if nu.op == "unfold":
+                return nu.attr["K"]
+            if nu.op == "softmax":
+                return 3
+            if nu.op == "fc":
+                o, k = self.g.fc_shape(u)
+                return o if min(o, k) <= SMALL_FC else tc_tile(o)[1]
+            return 1
+
+        def loads(v, seen=None):
+            seen = set() if seen is None else seen
+            if v in seen:
+                return 0
+            seen.add(v)
+            if mat(v):
+                return 1
+            return sum(loads(i, seen) for i in self.nodes[v].ins)
+
+        for v in range(len(self.nodes) - 1, 0, -1):
+            nd = self.nodes[v]
+            evals[v] = sum(factor(u, pos) * (1 if mat(u) else evals.get(u, 1)) for u, pos in nd.consumers) or 1
+            if nd.op in ("ew", "bcast") and v != self.out and evals[v] >= REPLICATE_MIN and loads(v) >= 2:
+                chosen.add(v)
+                evals[v] = 1
+        return chosen
 
     # -------------------------------------------------------------- descriptors
     @staticmethod
