@@ -337,6 +337,21 @@ __device__ __forceinline__ void tmem_ld16(cv_u32 taddr, float* v) {
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+__device__ __forceinline__ void tmem_ld32(cv_u32 taddr, float* v) {
+  cv_u32 r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 template <int N>
 struct TmemCols {
   static constexpr int value = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
@@ -591,6 +606,201 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   fence_before();
   __syncthreads();
   if (warp == kProducerWarps) {
+    fence_after();
+    tmem_free<NCOLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent FC forward / dgrad (tcgen05, 3xTF32).  Same math and operand
+// layouts as tc_gemm_pix<..., PACKED=true, A_MN=true>, but each CTA walks a
+// strided list of (pixel tile, column tile) work items with two TMEM
+// accumulators, so the epilogue of tile i (dedicated warps) overlaps the
+// producer/MMA mainloop of tile i+1.  Warp roles: PW producer warps, 1 MMA
+// warp, 1 TMA bulk-copy warp (packed weight images), 4 epilogue warps (one
+// per TMEM lane quadrant).
+// ---------------------------------------------------------------------------
+template <int NT, int STAGES>
+struct SmemP {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = NT * 128;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+template <class F, int NT, int STAGES, int PW, int EW>
+__device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
+  using namespace tc;
+  using L = SmemP<NT, STAGES>;
+  constexpr int NCOLS = TmemCols<2 * NT>::value;
+  constexpr int KB = (F::K + kBK - 1) / kBK;
+  constexpr int NCT = (F::M + NT - 1) / NT;
+  constexpr int ROWS = kBK / PW;  // k-rows per producer warp per k-block
+  static_assert(kBK % PW == 0, "producer warps must divide the k-block");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((unsigned long long)smem_raw + 1023) & ~1023ull);
+  cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
+  cv_u64* empty = full + STAGES;
+  cv_u64* tfull = empty + STAGES;   // [2]
+  cv_u64* tempty = tfull + 2;       // [2]
+  cv_u32* tslot = (cv_u32*)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long T = a.n * (long long)F::S;
+  const long long PT = (T + kBM - 1) / kBM;
+  const long long TILES = PT * NCT;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], PW * 32 + 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], EW * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == PW) tmem_alloc<NCOLS>(tslot);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const cv_u32 tmem = *tslot;
+
+  if (warp < PW) {
+    // ---- producers: MN-major computed operand, warp owns ROWS k-rows, lane = pixel
+    long long g = 0;  // global k-block counter (ring position)
+    for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x) {
+      const long long t0 = (tile / NCT) * kBM;
+      int pn[4], ps[4];
+      unsigned okmask = 0;
+#pragma unroll
+      for (int mb = 0; mb < 4; ++mb) {
+        const long long t = t0 + mb * 32 + lane;
+        okmask |= (t < T ? 1u : 0u) << mb;
+        const long long tc = t < T ? t : T - 1;
+        pn[mb] = (int)(tc / F::S);
+        ps[mb] = (int)(tc - (long long)pn[mb] * F::S);
+      }
+      float va[ROWS][4];
+      auto gather = [&](int kb) {
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+          const int k = kb * kBK + warp * ROWS + q;
+          const int kc = k < F::K ? k : F::K - 1;
+#pragma unroll
+          for (int mb = 0; mb < 4; ++mb) {
+            const float v = F::B(a, (long long)pn[mb], kc, ps[mb]);
+            va[q][mb] = (((okmask >> mb) & 1u) && k < F::K) ? v : 0.f;
+          }
+        }
+      };
+      gather(0);
+      for (int kb = 0; kb < KB; ++kb, ++g) {
+        const int st = (int)(g % STAGES);
+        if (g >= STAGES) mbar_wait(&empty[st], (cv_u32)(((g / STAGES) & 1) ^ 1));
+        uint8_t* sa_hi = smem + st * L::STAGE;
+        uint8_t* sa_lo = sa_hi + L::A_BYTES;
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q)
+#pragma unroll
+          for (int mb = 0; mb < 4; ++mb) {
+            float h, l;
+            split_tf32(va[q][mb], h, l);
+            const int off = mn_off(mb * 32 + lane, warp * ROWS + q);
+            *reinterpret_cast<float*>(sa_hi + off) = h;
+            *reinterpret_cast<float*>(sa_lo + off) = l;
+          }
+        fence_async_smem();
+        mbar_arrive(&full[st]);
+        if (kb + 1 < KB) gather(kb + 1);
+      }
+    }
+  } else if (warp == PW) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      constexpr cv_u32 idesc = idesc_tf32(NT, true);
+      long long g = 0;
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        if (it >= 2) mbar_wait(&tempty[buf], (cv_u32)(((it >> 1) & 1) ^ 1));
+        fence_after();
+        const cv_u32 d = tmem + buf * NT;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int st = (int)(g % STAGES);
+          mbar_wait(&full[st], (cv_u32)((g / STAGES) & 1));
+          fence_after();
+          const cv_u32 a_hi = smem_u32(smem + st * L::STAGE);
+          const cv_u32 a_lo = a_hi + L::A_BYTES;
+          const cv_u32 b_hi = a_lo + L::A_BYTES;
+          const cv_u32 b_lo = b_hi + L::B_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 8; ++kk) {
+            const cv_u64 dah = desc_mn_sw128_32b(a_hi + kk * 4096, 512, 2048);
+            const cv_u64 dal = desc_mn_sw128_32b(a_lo + kk * 4096, 512, 2048);
+            mma_tf32(d, dah, desc_k_sw128(b_hi + kk * 32), idesc, (kb | kk) != 0);
+            mma_tf32(d, dah, desc_k_sw128(b_lo + kk * 32), idesc, 1);
+            mma_tf32(d, dal, desc_k_sw128(b_hi + kk * 32), idesc, 1);
+          }
+          commit(&empty[st]);
+        }
+        commit(&tfull[buf]);
+      }
+    }
+  } else if (warp == PW + 1) {
+    // ---- TMA bulk loader of the packed weight tile images
+    if (lane == 0) {
+      const uint8_t* img0 = reinterpret_cast<const uint8_t*>(F::packed(a));
+      long long g = 0;
+      for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x) {
+        const int ct = (int)(tile % NCT);
+        const uint8_t* img = img0 + (long long)ct * KB * 2 * L::B_BYTES;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int st = (int)(g % STAGES);
+          if (g >= STAGES) mbar_wait(&empty[st], (cv_u32)(((g / STAGES) & 1) ^ 1));
+          mbar_arrive_tx(&full[st], 2 * L::B_BYTES);
+          bulk_g2s(smem + st * L::STAGE + 2 * L::A_BYTES, img + (long long)kb * 2 * L::B_BYTES, 2 * L::B_BYTES, &full[st]);
+        }
+      }
+    }
+  } else {
+    // ---- epilogue: warp quadrant q = warp % 4 owns accumulator rows 32q..32q+31;
+    // with EW = 8 the two warpgroups split the columns
+    const int q = warp & 3;
+    const int part = (warp - PW - 2) >> 2;  // 0 .. EW/4-1
+    constexpr int CPART = ((NT / (EW / 4)) + 31) / 32 * 32;
+    int it = 0;
+    for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const long long t0 = (tile / NCT) * kBM;
+      const int c0 = (int)(tile % NCT) * NT;
+      mbar_wait(&tfull[buf], (cv_u32)((it >> 1) & 1));
+      fence_after();
+      const long long te = t0 + q * 32 + lane;
+      const bool eok = te < T;
+      const long long en = eok ? te / F::S : 0;
+      const int es = eok ? (int)(te - en * F::S) : 0;
+      const int cb = part * CPART;
+#pragma unroll 1
+      for (int cc = cb; cc < cb + CPART && cc < NT; cc += 32) {
+        float v[32];
+        tmem_ld32(tmem + buf * NT + ((cv_u32)(q * 32) << 16) + cc, v);
+        if (eok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int col = c0 + cc + j;
+            if (cc + j < NT && col < F::M) F::store(a, en, col, es, v[j]);
+          }
+        }
+      }
+      fence_before();
+      mbar_arrive(&tempty[buf]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == PW) {
     fence_after();
     tmem_free<NCOLS>(tmem);
   }

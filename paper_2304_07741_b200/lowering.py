@@ -58,18 +58,29 @@ TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-co
 TC_SMEM_BUDGET = 200 * 1024
 TC_SMEM_PAIR = 110 * 1024 if os.environ.get("CANVAS_TC_PAIR", "1") == "1" else 0  # two CTAs/SM when a 2-stage ring fits
 TC_A_MN = "true" if os.environ.get("CANVAS_TC_AMN", "1") == "1" else "false"  # computed operand layout
+TC_NTMAX = int(os.environ.get("CANVAS_TC_NTMAX", "256"))  # widest MMA N tile
+TC_PERSIST = os.environ.get("CANVAS_TC_PERSIST", "1") == "1"  # persistent fwd/dgrad GEMMs
+TC_PW = int(os.environ.get("CANVAS_TC_PW", "8"))  # producer warps of the persistent GEMM
+SMS = 148
 TC_WGRAD_TCHUNK = 4096  # pixels per wgrad split (128 k-blocks of 32)
 
 
 def tc_tile(cols: int) -> tuple[int, int, int]:
     """(NT, number of column tiles, pipeline stages) for an MMA N extent of ``cols``."""
-    nct = -(-cols // 256)
+    nct = -(-cols // TC_NTMAX)
     nt = -(-(-(-cols // nct)) // 16) * 16
     stage = 2 * 128 * 128 + 2 * nt * 128
     if 2 * stage + 2048 <= TC_SMEM_PAIR:
         return nt, nct, 2
     stages = max(2, min(4, TC_SMEM_BUDGET // stage))
     return nt, nct, stages
+
+
+def tc_persist_cfg(nt: int) -> tuple[int, int]:
+    """(stages, smem bytes) of tc_gemm_pix_persistent (must match canvas::SmemP)."""
+    stage = 2 * 128 * 128 + 2 * nt * 128
+    stages = max(2, min(6, (220 * 1024) // stage))
+    return stages, stages * stage + (2 * stages + 4) * 8 + 16 + 1024
 
 
 def tc_smem_bytes(nt: int, stages: int) -> int:
@@ -992,6 +1003,19 @@ class Lowerer:
                 pslot = -1 - k_ws
             ploc = fa.ptr(pslot)
             functor = functor[: functor.rindex("};")] + f"  static __device__ __forceinline__ float* packed(const CanvasArgs& a) {{ return {ploc}; }}\n}};\n"
+            if TC_PERSIST and K < 4 * nt:  # epilogue-heavy: overlap stores with the next tile
+                pstages, psmem = tc_persist_cfg(nt)
+                pw = TC_PW if K > 128 else 4  # short reductions: cheap mainloop, store-bound epilogue
+                ew = 8 if nt >= 128 else 4
+                threads = (pw + 2 + ew) * 32
+                launcher = f'extern "C" __global__ void __launch_bounds__({threads}, 1) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_persistent<{name}_F, {nt}, {pstages}, {pw}, {ew}>(a); }}\n'
+                k = self.add_kernel(name, functor, launcher)
+                pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
+                total = nct * kb * nt * 32
+                self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
+                grid = (GridRule(S * nct, 0, 128, SMS), GridRule(0, 1, 1), GridRule(0, 1, 1))
+                self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=psmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+                return
             launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true, {TC_A_MN}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')

@@ -91,6 +91,8 @@ template <class F, int NT, int STAGES, bool PACKED, bool A_MN>
 void tc_gemm_pix(const CanvasArgs& a) { gemm_nk<F>(a); }
 template <class F, int NT>
 void tc_pack_b(const CanvasArgs&) {}
+template <class F, int NT, int STAGES, int PW, int EW>
+void tc_gemm_pix_persistent(const CanvasArgs& a) { gemm_nk<F>(a); }
 template <class F, int NT, int STAGES>
 void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 }  // namespace canvas
