@@ -41,14 +41,17 @@ namespace canvas {
 // ---------------------------------------------------------------------------
 // K1/K2: pointwise maps, folds and softmax rows
 // ---------------------------------------------------------------------------
-template <class F>
+// V > 1: each thread evaluates V consecutive elements (PER % V == 0), so the
+// V independent gathers are in flight together and shared index math is reused.
+template <class F, int V = 1>
 __device__ __forceinline__ void pointwise(const CanvasArgs& a) {
-  const long long total = a.n * F::PER;
+  const long long total = a.n * (F::PER / V);
   const long long step = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += step) {
-    const long long n = i / F::PER;
-    const int r = (int)(i - n * F::PER);
-    F::run(a, n, r);
+    const long long n = i / (F::PER / V);
+    const int r = (int)(i - n * (F::PER / V)) * V;
+#pragma unroll
+    for (int j = 0; j < V; ++j) F::run(a, n, r + j);
   }
 }
 

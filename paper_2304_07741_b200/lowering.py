@@ -49,6 +49,7 @@ SLOT_X, SLOT_Y, SLOT_DY, SLOT_DX = 0, 1, 2, 3
 BETA_NONE, BETA_AFTER_FIRST, BETA_ALWAYS = 0, 1, 2
 
 POINTWISE_BLOCK = 256
+POINTWISE_VEC = int(os.environ.get("CANVAS_PW_VEC", "4"))  # elements per thread along the innermost dim
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
 GEMM_TILE = 64
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
@@ -342,21 +343,38 @@ class Fn:
         return r
 
     def offset(self, d: TDesc, coords) -> str:
-        coords, strides = list(coords), list(d.strides)
-        # a suffix of coordinates that is the decomposition of a flat index over
-        # contiguous dims collapses back to that index (e.g. (h, w) -> s)
-        for L in range(len(coords), 1, -1):
-            got = self.flat_of.get(tuple(coords[-L:]))
-            if got is None:
+        """Element offset sum(coord_i * stride_i) as an affine form over base
+        coordinates, with every run of coordinates that came from decomposing a
+        flat index (over contiguous strides) folded back into that index — e.g.
+        (h+1)*W + (w+1) -> s + W + 1, (g*(C/G) + j)*S -> c*S."""
+        acc: dict = {}
+        const = 0
+        for c, st in zip(coords, d.strides):
+            if st == 0:
                 continue
-            flat, ext = got
-            st = strides[-L:]
-            contig = all(st[i] == st[i + 1] * ext[i + 1] for i in range(L - 1))
-            if tuple(ext) == tuple(d.dims[-L:]) and contig:
-                coords = coords[:-L] + [flat]
-                strides = strides[:-L] + [st[-1]]
+            t, k = self.lin(c)
+            const += k * st
+            for v, q in t.items():
+                acc[v] = acc.get(v, 0) + q * st
+        for dec, (flat, ext) in sorted(self.flat_of.items(), key=lambda kv: -len(kv[0])):
+            L = len(dec)
+            for j in range(L - 1):  # window dec[j:], longest first
+                vars_ = [(v, e) for v, e in zip(dec[j:], ext[j:])]
+                live = [(i, v) for i, (v, e) in enumerate(vars_) if v != "0" and e > 1]
+                if len(live) < 2 or any(v not in acc for _, v in live):
+                    continue
+                inner = [math.prod(e for _, e in vars_[i + 1 :]) for i in range(len(vars_))]
+                alpha = acc[live[-1][1]] // inner[live[-1][0]] if acc[live[-1][1]] % inner[live[-1][0]] == 0 else None
+                if alpha is None or any(acc[v] != alpha * inner[i] for i, v in live):
+                    continue
+                sub = flat if j == 0 else self.ivar(f"{flat} % {math.prod(ext[j:])}")
+                for _, v in live:
+                    del acc[v]
+                acc[sub] = acc.get(sub, 0) + alpha
                 break
-        terms = [f"{c}*{s}" if s != 1 else f"{c}" for c, s in zip(coords, strides) if s != 0 and c != "0"]
+        terms = [f"{v}" if k == 1 else f"{v}*{k}" for v, k in sorted(acc.items(), key=lambda kv: -abs(kv[1])) if k]
+        if const:
+            terms.append(f"({const})")
         return self.ivar(" + ".join(terms) if terms else "0")
 
     def addr(self, d: TDesc, coords) -> str:
@@ -788,11 +806,13 @@ class Lowerer:
         src += ["  }", "};"]
         return "\n".join(src) + "\n", f.local_slots
 
-    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0):
+    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1):
+        """``inner``: extent of the innermost output dim (per-thread vector width must divide it)."""
         functor, slots = self.functor_pointwise(name, per_image, body_fn)
-        launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F>(a); }}\n'
+        v = next((c for c in (POINTWISE_VEC, 2) if c > 1 and inner % c == 0 and per_image % c == 0), 1)
+        launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {v}>(a); }}\n'
         k = self.add_kernel(name, functor, launcher)
-        grid = (GridRule(per_image, 0, POINTWISE_BLOCK, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        grid = (GridRule(per_image // v, 0, POINTWISE_BLOCK, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
         self.p.launches.append(Launch("kernel", phase, name, k, POINTWISE_BLOCK, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
 
     # ---- forward
@@ -827,15 +847,16 @@ class Lowerer:
             tg = self.fwd_targets(v)
             io = 4 * (nd.numel + self._input_numel(nd))
             if nd.op == "fold":
-                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_fold(f, v, tg), 0, beta, f"fold {nd.attr['mode']} -> n{v}", io, 0)
+                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_fold(f, v, tg), 0, beta, f"fold {nd.attr['mode']} -> n{v}", io, 0, inner=nd.ext[-1] if nd.ext else 1)
             elif nd.op == "softmax":
                 pre, span, post = self.softmax_geom(nd)
                 rows = math.prod(pre) * math.prod(post)
-                self.launch_pointwise(name, rows, lambda f, v=v, tg=tg: self.body_softmax(f, v, tg), 0, beta, f"softmax -> n{v}", io, 0)
+                rext = pre + post
+                self.launch_pointwise(name, rows, lambda f, v=v, tg=tg: self.body_softmax(f, v, tg), 0, beta, f"softmax -> n{v}", io, 0, inner=rext[-1] if rext else 1)
             elif nd.op == "fc":
                 self.lower_fc_fwd(name, v, tg, beta)
             else:
-                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_map(f, v, tg), 0, beta, f"pointwise -> n{v}", io, 0)
+                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_map(f, v, tg), 0, beta, f"pointwise -> n{v}", io, 0, inner=nd.ext[-1] if nd.ext else 1)
 
     def _input_numel(self, nd) -> int:
         """Compulsory reads: materialised tensors the node's expression touches (once each)."""
@@ -945,7 +966,7 @@ class Lowerer:
                 for d, b in targets:
                     f.store(d, c, acc, b)
 
-            self.launch_pointwise(name, nu.numel, body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops)
+            self.launch_pointwise(name, nu.numel, body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1)
             return
         # A(m,k) = W[m*K + k];  B(n,k,s) = val(v)(decompose k | decompose s)
         fa = Fn(self)
@@ -1118,7 +1139,7 @@ class Lowerer:
                 beta = dx_beta if u == 0 else BETA_NONE
                 d = self.grad_desc[u]
                 name = f"k{len(p.kernel_names)}_bwd_grad{u}"
-                self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0)
+                self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0, inner=nu.ext[-1] if nu.ext else 1)
             # 2) adjoint kernels of the producer edge that need dL/du as a whole
             if nu.op == "fc":
                 self.lower_fc_bwd(u, dx_beta)
@@ -1159,7 +1180,8 @@ class Lowerer:
             f.store(d, pc + qc, acc, False)
 
         name = f"k{len(self.p.kernel_names)}_bwd_softmaxdot{u}"
-        self.launch_pointwise(name, rows, body, 1, BETA_NONE, f"softmax row-dot n{u}", 4 * (2 * nu.numel + rows), 0)
+        rext = pre + post
+        self.launch_pointwise(name, rows, body, 1, BETA_NONE, f"softmax row-dot n{u}", 4 * (2 * nu.numel + rows), 0, inner=rext[-1] if rext else 1)
 
     def lower_fc_bwd(self, u: int, dx_beta: int) -> None:
         nu = self.nodes[u]
@@ -1188,7 +1210,7 @@ class Lowerer:
                 f.close()
                 f.store(dd, c, acc, beta != BETA_NONE)
 
-            self.launch_pointwise(name, nv.numel, body, 1, beta, f"dgrad_small {O}x{K} n{u}->n{v}", 4 * (nu.numel + nv.numel), flops)
+            self.launch_pointwise(name, nv.numel, body, 1, beta, f"dgrad_small {O}x{K} n{u}->n{v}", 4 * (nu.numel + nv.numel), flops, inner=nv.ext[-1] if nv.ext else 1)
         else:
             fa = Fn(self)
             fa.pre = []

@@ -31,7 +31,7 @@ struct CanvasArgs {
 };
 
 namespace canvas {
-template <class F>
+template <class F, int V = 1>
 void pointwise(const CanvasArgs& a) {
   for (long long n = 0; n < a.n; ++n)
     for (int r = 0; r < (int)F::PER; ++r) F::run(a, n, r);
