@@ -41,17 +41,21 @@ namespace canvas {
 // ---------------------------------------------------------------------------
 // K1/K2: pointwise maps, folds and softmax rows
 // ---------------------------------------------------------------------------
-// V > 1: each thread evaluates V consecutive elements (PER % V == 0), so the
-// V independent gathers are in flight together and shared index math is reused.
+// V > 1: each thread evaluates V elements blockDim apart (every load instruction
+// stays coalesced), giving V independent gathers per thread.
 template <class F, int V = 1>
 __device__ __forceinline__ void pointwise(const CanvasArgs& a) {
-  const long long total = a.n * (F::PER / V);
-  const long long step = (long long)gridDim.x * blockDim.x;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += step) {
-    const long long n = i / (F::PER / V);
-    const int r = (int)(i - n * (F::PER / V)) * V;
+  const long long total = a.n * F::PER;
+  const long long chunk = (long long)blockDim.x * V;
+  for (long long base = (long long)blockIdx.x * chunk; base < total; base += (long long)gridDim.x * chunk) {
 #pragma unroll
-    for (int j = 0; j < V; ++j) F::run(a, n, r + j);
+    for (int j = 0; j < V; ++j) {
+      const long long i = base + j * blockDim.x + threadIdx.x;
+      if (i < total) {
+        const long long n = i / F::PER;
+        F::run(a, n, (int)(i - n * F::PER));
+      }
+    }
   }
 }
 

@@ -49,7 +49,7 @@ SLOT_X, SLOT_Y, SLOT_DY, SLOT_DX = 0, 1, 2, 3
 BETA_NONE, BETA_AFTER_FIRST, BETA_ALWAYS = 0, 1, 2
 
 POINTWISE_BLOCK = 256
-POINTWISE_VEC = int(os.environ.get("CANVAS_PW_VEC", "4"))  # elements per thread along the innermost dim
+POINTWISE_VEC = int(os.environ.get("CANVAS_PW_VEC", "1"))  # elements per thread along the innermost dim
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
 GEMM_TILE = 64
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
@@ -809,10 +809,10 @@ class Lowerer:
     def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1):
         """``inner``: extent of the innermost output dim (per-thread vector width must divide it)."""
         functor, slots = self.functor_pointwise(name, per_image, body_fn)
-        v = next((c for c in (POINTWISE_VEC, 2) if c > 1 and inner % c == 0 and per_image % c == 0), 1)
+        v = POINTWISE_VEC
         launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {v}>(a); }}\n'
         k = self.add_kernel(name, functor, launcher)
-        grid = (GridRule(per_image // v, 0, POINTWISE_BLOCK, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        grid = (GridRule(per_image, 0, POINTWISE_BLOCK * v, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
         self.p.launches.append(Launch("kernel", phase, name, k, POINTWISE_BLOCK, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
 
     # ---- forward
