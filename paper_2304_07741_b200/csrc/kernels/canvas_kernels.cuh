@@ -237,9 +237,9 @@ __device__ __forceinline__ void mbar_wait(cv_u64* bar, cv_u32 parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "r"(0x989680)  // suspend-time hint: sleep instead of spinning on issue slots
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_tx(cv_u64* bar, cv_u32 bytes) {
@@ -256,13 +256,13 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// split x into (hi, lo) tf32 bit patterns
+// split x into (hi, lo): hi keeps the 10 explicit tf32 mantissa bits (mask),
+// lo = x - hi is exact in fp32 and is itself read as tf32 by the tensor core.
+// hi*hi + hi*lo + lo*hi then carries ~2^-20 relative error per product — the
+// 3xTF32 scheme at 2 instructions instead of two cvt.rna emulations.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  cv_u32 h, l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
-  lo = __uint_as_float(l);
+  hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+  lo = x - hi;
 }
 
 __device__ __forceinline__ void st_shared_v4(void* p, float a, float b, float c, float d) {
@@ -889,16 +889,23 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     constexpr int RA = kBM / 32, RB = (NT + 31) / 32;
     float va[RA][4], vb[RB][4];
     auto gather = [&](int kb) {
+      // 4 consecutive pixels: one 32-bit divide, then carry across the image edge
       long long nn[4];
       int ss[4];
       bool okk[4];
+      const long long tq = tbeg + (long long)kb * kBK + c * 4;
+      const unsigned tq32 = (unsigned)(tq < tend ? tq : tbeg);
+      int n0 = (int)(tq32 / (unsigned)F::S);
+      int s0 = (int)(tq32 - (unsigned)n0 * (unsigned)F::S);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const long long t = tbeg + (long long)kb * kBK + c * 4 + j;
-        okk[j] = t < tend;
-        const long long tc = okk[j] ? t : tbeg;
-        nn[j] = tc / F::S;
-        ss[j] = (int)(tc - nn[j] * F::S);
+        okk[j] = tq + j < tend;
+        nn[j] = okk[j] ? n0 : (int)(tq32 / (unsigned)F::S);
+        ss[j] = okk[j] ? s0 : (int)(tq32 - (unsigned)nn[j] * (unsigned)F::S);
+        if (++s0 == F::S) {
+          s0 = 0;
+          ++n0;
+        }
       }
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
