@@ -889,23 +889,16 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     constexpr int RA = kBM / 32, RB = (NT + 31) / 32;
     float va[RA][4], vb[RB][4];
     auto gather = [&](int kb) {
-      // 4 consecutive pixels: one 32-bit divide, then carry across the image edge
       long long nn[4];
       int ss[4];
       bool okk[4];
-      const long long tq = tbeg + (long long)kb * kBK + c * 4;
-      const unsigned tq32 = (unsigned)(tq < tend ? tq : tbeg);
-      int n0 = (int)(tq32 / (unsigned)F::S);
-      int s0 = (int)(tq32 - (unsigned)n0 * (unsigned)F::S);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        okk[j] = tq + j < tend;
-        nn[j] = okk[j] ? n0 : (int)(tq32 / (unsigned)F::S);
-        ss[j] = okk[j] ? s0 : (int)(tq32 - (unsigned)nn[j] * (unsigned)F::S);
-        if (++s0 == F::S) {
-          s0 = 0;
-          ++n0;
-        }
+        const long long t = tbeg + (long long)kb * kBK + c * 4 + j;
+        okk[j] = t < tend;
+        const long long tc = okk[j] ? t : tbeg;
+        nn[j] = tc / F::S;
+        ss[j] = (int)(tc - nn[j] * F::S);
       }
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
