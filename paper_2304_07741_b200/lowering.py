@@ -284,6 +284,11 @@ class Fn:
     def memo_put(self, key, val) -> None:
         self.scopes[-1][key] = val
 
+    def loop(self, var: str, trip: int) -> None:
+        """Counted loop; short trips unrolled fully (independent gathers in flight), long ones by 4."""
+        self.emit("#pragma unroll" if trip <= 16 else "#pragma unroll 4")
+        self.open(f"for (int {var} = 0; {var} < {trip}; ++{var})")
+
     def open(self, head: str) -> None:
         self.emit(head + " {")
         self.indent += 1
@@ -768,7 +773,7 @@ class Lowerer:
                 acc = f.fresh("s")
                 f.emit(f"float {acc} = 0.f;")
                 mv = f.fresh("m")
-                f.open(f"for (int {mv} = 0; {mv} < {M}; ++{mv})")
+                f.loop(mv, M)
                 t = term(mv)
                 f.emit(f"{acc} += {t};")
                 f.close()
@@ -894,7 +899,7 @@ class Lowerer:
             cnt = f.fresh("cnt")
             f.emit(f"float {acc} = -INFINITY; float {cnt} = 0.f;")
         j = f.fresh("j")
-        f.open(f"for (int {j} = 0; {j} < {D}; ++{j})")
+        f.loop(j, D)
         x = self.val(f, nd.ins[0], c[:dim] + (j,) + c[dim:])
         if mode == "avg":
             f.emit(f"{acc} += {x};")
@@ -918,7 +923,7 @@ class Lowerer:
 
         def loop(stmt_fn):
             j = f.fresh("j")
-            f.open(f"for (int {j} = 0; {j} < {S}; ++{j})")
+            f.loop(j, S)
             sc = tuple(f.decompose(j, span))
             c = pc + sc + qc
             x = self.val(f, nd.ins[0], c)
@@ -958,7 +963,7 @@ class Lowerer:
                 f.emit(f"float {acc} = 0.f;")
                 wrow = f.ivar(f"{o}*{K}")
                 i = f.fresh("i")
-                f.open(f"for (int {i} = 0; {i} < {K}; ++{i})")
+                f.loop(i, K)
                 ch = tuple(f.decompose(i, nv.ch_ext))
                 x = self.val(f, v, ch + sp)
                 f.emit(f"{acc} = fmaf(__ldg({f.ptr(wslot)} + {wrow} + {i}), {x}, {acc});")
@@ -1171,7 +1176,7 @@ class Lowerer:
             acc = f.fresh("acc")
             f.emit(f"float {acc} = 0.f;")
             j = f.fresh("j")
-            f.open(f"for (int {j} = 0; {j} < {S}; ++{j})")
+            f.loop(j, S)
             c = pc + tuple(f.decompose(j, span)) + qc
             g = self.grad(f, u, c)
             y = self.val(f, u, c)
@@ -1204,7 +1209,7 @@ class Lowerer:
                 acc = f.fresh("acc")
                 f.emit(f"float {acc} = 0.f;")
                 o = f.fresh("o")
-                f.open(f"for (int {o} = 0; {o} < {O}; ++{o})")
+                f.loop(o, O)
                 g = self.grad(f, u, (o,) + sp)
                 f.emit(f"{acc} = fmaf(__ldg({f.ptr(wslot)} + {o}*{K} + {i}), {g}, {acc});")
                 f.close()
