@@ -422,8 +422,10 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
 // MMA rows = 128 pixels t = n*S + s (operand B(n,k,s), computed), MMA cols =
 // NT output channels (operand A(m,k), weights).
 // ---------------------------------------------------------------------------
-template <class F, int NT, int STAGES, bool PACKED, bool A_MN>
+template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = tc::kProducerWarps>
 __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
+  static_assert(A_MN || PW == tc::kProducerWarps, "K-major producer mapping assumes 8 warps");
+  static_assert(32 % PW == 0 && PW % 4 == 0, "PW must divide the k-block and cover the TMEM quadrants");
   using namespace tc;
   using L = Smem<NT, STAGES>;
   constexpr int NCOLS = TmemCols<NT>::value;
@@ -438,13 +440,13 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], kProducerWarps * 32 + (PACKED ? 1 : 0));
+      mbar_init(&full[i], PW * 32 + (PACKED ? 1 : 0));
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProducerWarps) tmem_alloc<NCOLS>(tslot);
+  if (warp == PW) tmem_alloc<NCOLS>(tslot);
   fence_before();
   __syncthreads();
   fence_after();
@@ -454,7 +456,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   const long long t0 = (long long)blockIdx.x * kBM;
   const int c0 = blockIdx.y * NT;
 
-  if (warp < kProducerWarps) {
+  if (warp < PW) {
     const int p = threadIdx.x;  // 0..255
     if (A_MN) {
       // MN-major A: warp w owns k-rows 4w..4w+3 of the 32-wide k-block, lane =
@@ -471,11 +473,12 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         pn[mb] = (int)(tc / F::S);
         ps[mb] = (int)(tc - (long long)pn[mb] * F::S);
       }
-      float va[4][4];
+      constexpr int ROWS = kBK / PW;
+      float va[ROWS][4];
       auto gather = [&](int kb) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k = kb * kBK + warp * 4 + q;
+        for (int q = 0; q < ROWS; ++q) {
+          const int k = kb * kBK + warp * ROWS + q;
           const int kc = k < F::K ? k : F::K - 1;
 #pragma unroll
           for (int mb = 0; mb < 4; ++mb) {
@@ -491,12 +494,12 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         uint8_t* sa_hi = smem + st * L::STAGE;
         uint8_t* sa_lo = sa_hi + L::A_BYTES;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < ROWS; ++q)
 #pragma unroll
           for (int mb = 0; mb < 4; ++mb) {
             float h, l;
             split_tf32(va[q][mb], h, l);
-            const int off = mn_off(mb * 32 + lane, warp * 4 + q);
+            const int off = mn_off(mb * 32 + lane, warp * ROWS + q);
             *reinterpret_cast<float*>(sa_hi + off) = h;
             *reinterpret_cast<float*>(sa_lo + off) = l;
           }
@@ -583,7 +586,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
     const bool eok = te < T;
     const long long en = eok ? te / F::S : 0;
     const int es = eok ? (int)(te - en * F::S) : 0;
-    constexpr int HALF = ((NT + 31) / 32) * 16;  // columns per warpgroup, multiple of 16
+    constexpr int HALF = ((NT + 16 * (PW / 4) - 1) / (16 * (PW / 4))) * 16;  // columns per warpgroup, multiple of 16
     const int cbeg = (warp >> 2) * HALF;
     for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {
       float v[16];
@@ -596,7 +599,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         }
       }
     }
-  } else if (warp == kProducerWarps) {
+  } else if (warp == PW) {
     if (lane == 0) mma_loop<NT, STAGES, A_MN>(smem, full, empty, done, tmem, KB);
   } else if (PACKED && lane == 0) {
     // B operand: pre-split, pre-swizzled weight tile images (tc_pack_b), one
@@ -612,7 +615,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   }
   fence_before();
   __syncthreads();
-  if (warp == kProducerWarps) {
+  if (warp == PW) {
     fence_after();
     tmem_free<NCOLS>(tmem);
   }
@@ -848,7 +851,7 @@ __device__ __forceinline__ void tc_pack_b(const CanvasArgs& a) {
 // m (operand A), reduction over a TCHUNK slice of pixels t; partials are
 // summed in order by reduce_partials (deterministic).
 // ---------------------------------------------------------------------------
-template <class F, int NT, int STAGES>
+template <class F, int NT, int STAGES, int PW = tc::kProducerWarps>
 __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   using namespace tc;
   using L = Smem<NT, STAGES>;
@@ -863,13 +866,13 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], kProducerWarps * 32);
+      mbar_init(&full[i], PW * 32);
       mbar_init(&empty[i], 1);
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kProducerWarps) tmem_alloc<NCOLS>(tslot);
+  if (warp == PW) tmem_alloc<NCOLS>(tslot);
   fence_before();
   __syncthreads();
   fence_after();
@@ -882,45 +885,33 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   const int j0 = blockIdx.x * kBM;  // rows: input channels
   const int m0 = blockIdx.y * NT;   // cols: output channels
 
-  if (warp < kProducerWarps) {
-    const int p = threadIdx.x;  // 0..255
-    const int c = p & 7;        // 16 B chunk = 4 consecutive pixels
-    const int rsub = p >> 3;    // 0..31: row within a 32-row pass
-    constexpr int RA = kBM / 32, RB = (NT + 31) / 32;
-    float va[RA][4], vb[RB][4];
+  if (warp < PW) {
+    // lane = pixel of the 32-pixel k-block (coalesced gathers, one pixel
+    // decomposition per k-block); warp w owns rows w, w+8, ... (channel index
+    // math is warp-uniform); each warp writes whole 128 B swizzled rows.
+    constexpr int RA = kBM / PW, RB = (NT + PW - 1) / PW;
+    float va[RA], vb[RB];
     auto gather = [&](int kb) {
-      long long nn[4];
-      int ss[4];
-      bool okk[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const long long t = tbeg + (long long)kb * kBK + c * 4 + j;
-        okk[j] = t < tend;
-        const long long tc = okk[j] ? t : tbeg;
-        nn[j] = tc / F::S;
-        ss[j] = (int)(tc - nn[j] * F::S);
-      }
+      const long long t = tbeg + (long long)kb * kBK + lane;
+      const bool ok = t < tend;
+      const long long tc = ok ? t : tbeg;
+      const long long n = tc / F::S;
+      const int s = (int)(tc - n * F::S);
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
-        const int jj = j0 + rsub + 32 * w;
-        const int jc = jj < F::J ? jj : F::J - 1;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float v = F::B(a, nn[j], jc, ss[j]);
-          va[w][j] = (okk[j] && jj < F::J) ? v : 0.f;
-        }
+        const int jj = j0 + warp + PW * w;
+        const float v = F::B(a, n, jj < F::J ? jj : F::J - 1, s);
+        va[w] = (ok && jj < F::J) ? v : 0.f;
       }
 #pragma unroll
       for (int w = 0; w < RB; ++w) {
-        const int mm = m0 + rsub + 32 * w;
-        const int mc = mm < F::M ? mm : F::M - 1;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float v = F::A(a, nn[j], mc, ss[j]);
-          vb[w][j] = (okk[j] && mm < F::M && rsub + 32 * w < NT) ? v : 0.f;
-        }
+        const int row = warp + PW * w;
+        const int mm = m0 + row;
+        const float v = F::A(a, n, mm < F::M ? mm : F::M - 1, s);
+        vb[w] = (ok && mm < F::M && row < NT) ? v : 0.f;
       }
     };
+    const int off_l = ((lane >> 2) << 4) | ((lane & 3) << 2);  // chunk/word of this pixel before the swizzle
     if (KB > 0) gather(0);
     for (int kb = 0; kb < KB; ++kb) {
       const int st = kb % STAGES;
@@ -931,23 +922,22 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       uint8_t* sb_lo = sb_hi + L::B_BYTES;
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
-        float h[4], l[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) split_tf32(va[w][j], h[j], l[j]);
-        const int off = swz(rsub + 32 * w, c);
-        *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        const int row = warp + PW * w;
+        const int off = row * 128 + (off_l ^ ((row & 7) << 4));
+        float h, l;
+        split_tf32(va[w], h, l);
+        *reinterpret_cast<float*>(sa_hi + off) = h;
+        *reinterpret_cast<float*>(sa_lo + off) = l;
       }
 #pragma unroll
       for (int w = 0; w < RB; ++w) {
-        const int row = rsub + 32 * w;
+        const int row = warp + PW * w;
         if (row < NT) {
-          float h[4], l[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) split_tf32(vb[w][j], h[j], l[j]);
-          const int off = swz(row, c);
-          *reinterpret_cast<float4*>(sb_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(sb_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+          const int off = row * 128 + (off_l ^ ((row & 7) << 4));
+          float h, l;
+          split_tf32(vb[w], h, l);
+          *reinterpret_cast<float*>(sb_hi + off) = h;
+          *reinterpret_cast<float*>(sb_lo + off) = l;
         }
       }
       fence_async_smem();
@@ -972,13 +962,13 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
         }
       }
     }
-  } else if (warp == kProducerWarps && lane == 0) {
+  } else if (warp == PW && lane == 0) {
     if (KB > 0) mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
     else tc::mbar_arrive(done);
   }
   fence_before();
   __syncthreads();
-  if (warp == kProducerWarps) {
+  if (warp == PW) {
     fence_after();
     tmem_free<NCOLS>(tmem);
   }

@@ -63,7 +63,9 @@ TC_NTMAX = int(os.environ.get("CANVAS_TC_NTMAX", "256"))  # widest MMA N tile
 TC_PERSIST = os.environ.get("CANVAS_TC_PERSIST", "1") == "1"  # persistent fwd/dgrad GEMMs
 TC_PW = int(os.environ.get("CANVAS_TC_PW", "8"))  # producer warps of the persistent GEMM
 SMS = 148
-TC_WGRAD_TCHUNK = 4096  # pixels per wgrad split (128 k-blocks of 32)
+TC_WGRAD_TCHUNK = 4096
+TC_WGRAD_PW = int(os.environ.get("CANVAS_WGRAD_PW", "16"))  # wgrad producer warps
+TC_PIX_PW = int(os.environ.get("CANVAS_PIX_PW", "0"))  # 0 = auto  # fwd/dgrad (non-persistent) producer warps  # pixels per wgrad split (128 k-blocks of 32)
 
 
 def tc_tile(cols: int) -> tuple[int, int, int]:
@@ -1042,13 +1044,20 @@ class Lowerer:
                 grid = (GridRule(S * nct, 0, 128, SMS), GridRule(0, 1, 1), GridRule(0, 1, 1))
                 self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=psmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
                 return
-            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true, {TC_A_MN}>(a); }}\n'
+            # 2 CTAs x 8 producer warps when a 2-stage ring pairs on an SM, else 1 CTA x 16 warps
+            pw = TC_PIX_PW if TC_PIX_PW else (8 if smem <= TC_SMEM_PAIR else 16)
+            threads = (pw + 2) * 32
+            if pw > 8:
+                stages = max(2, min(4, (220 * 1024) // (2 * 128 * 128 + 2 * nt * 128)))
+                smem = tc_smem_bytes(nt, stages)
+            pair = smem <= TC_SMEM_PAIR and pw <= 8
+            launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true, {TC_A_MN}, {pw}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
             total = nct * kb * nt * 32
             self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
             grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
-            self.p.launches.append(Launch("kernel", phase, name, k, TC_THREADS, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+            self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
             return
         launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_nk<{name}_F>(a); }}\n'
         k = self.add_kernel(name, functor, launcher)
@@ -1082,10 +1091,13 @@ class Lowerer:
         if use_tc:
             nt, nct, stages = tc_tile(M)
             smem = tc_smem_bytes(nt, stages)
-            launcher = f'extern "C" __global__ void __launch_bounds__({TC_THREADS}, {2 if smem <= TC_SMEM_PAIR else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}>(a); }}\n'
+            pw = TC_WGRAD_PW
+            threads = (pw + 2) * 32
+            pair = smem <= TC_SMEM_PAIR and pw <= 8
+            launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}, {pw}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             grid = (GridRule(0, J, 128), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
-            self.p.launches.append(Launch("kernel", 1, name, k, TC_THREADS, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+            self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
         else:
             launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_wgrad<{name}_F>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)

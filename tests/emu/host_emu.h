@@ -87,12 +87,12 @@ void reduce_partials(const CanvasArgs& a) {
     a.p[1][idx] = s;
   }
 }
-template <class F, int NT, int STAGES, bool PACKED, bool A_MN>
+template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = 8>
 void tc_gemm_pix(const CanvasArgs& a) { gemm_nk<F>(a); }
 template <class F, int NT>
 void tc_pack_b(const CanvasArgs&) {}
 template <class F, int NT, int STAGES, int PW, int EW>
 void tc_gemm_pix_persistent(const CanvasArgs& a) { gemm_nk<F>(a); }
-template <class F, int NT, int STAGES>
+template <class F, int NT, int STAGES, int PW = 8>
 void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 }  // namespace canvas
