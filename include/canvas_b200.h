@@ -85,12 +85,13 @@ int canvas_backward(const canvas_plan* p, int64_t batch, const float* x, const f
 
 /* Measurement hook: record CUDA events (CUevent / cudaEvent_t handles,
  * 2*n_pairs of them, start/end interleaved) around every launch of launch
- * record `record`, cycling through the pairs; n_pairs = 0 disables.  Used by
- * bench.py to time one kernel inside a full training step. */
+ * record `record`, cycling through the pairs; several records may be
+ * profiled at once; n_pairs = 0 disables that record.  Used by bench.py to
+ * time kernels inside a full training step. */
 int canvas_plan_profile(canvas_plan* p, int record, void* const* events, int n_pairs);
 
-/* Launches of the profiled record since canvas_plan_profile. */
-int64_t canvas_plan_profile_count(const canvas_plan* p);
+/* Launches of `record` recorded since its canvas_plan_profile. */
+int64_t canvas_plan_profile_count(const canvas_plan* p, int record);
 
 /* Message of the last failing call on this thread. */
 const char* canvas_last_error(void);

@@ -193,10 +193,12 @@ struct canvas_plan {
   std::vector<CUfunction> fns;
   // measurement hook (canvas_plan_profile): CUDA events recorded around every
   // launch of one record, so bench.py can time one kernel inside a full step
+  struct Prof {
+    std::vector<void*> events;  // 2 per slot: start, end
+    int64_t count = 0;
+  };
   mutable std::mutex prof_mu;
-  int64_t prof_record = -1;
-  std::vector<void*> prof_events;  // 2 per slot: start, end
-  mutable int64_t prof_count = 0;
+  mutable std::unordered_map<int64_t, Prof> prof;  // launch record -> event ring
 };
 
 namespace {
@@ -333,11 +335,15 @@ int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, co
       void* params[] = {&a};
       void* ev_end = nullptr;
       const int64_t ri = &r - p->recs.data();
-      if (ri == p->prof_record && !p->prof_events.empty()) {
+      if (!p->prof.empty()) {
         std::lock_guard<std::mutex> lk(p->prof_mu);
-        const size_t slot = (size_t)(p->prof_count++ % (int64_t)(p->prof_events.size() / 2));
-        d.cuEventRecord(p->prof_events[2 * slot], st);
-        ev_end = p->prof_events[2 * slot + 1];
+        auto it = p->prof.find(ri);
+        if (it != p->prof.end() && !it->second.events.empty()) {
+          auto& pr = it->second;
+          const size_t slot = (size_t)(pr.count++ % (int64_t)(pr.events.size() / 2));
+          d.cuEventRecord(pr.events[2 * slot], st);
+          ev_end = pr.events[2 * slot + 1];
+        }
       }
       CUresult e = d.cuLaunchKernel(p->fns[r.kernel], g[0], g[1], g[2], (unsigned)r.block, 1, 1, (unsigned)r.smem, st, params,
                                     nullptr);
@@ -490,13 +496,22 @@ int canvas_plan_profile(canvas_plan* p, int record, void* const* events, int n_p
   if (!p || record >= (int)p->recs.size() || n_pairs < 0 || (n_pairs && !events))
     return fail(CANVAS_ERR_ARGS, "bad profile request");
   std::lock_guard<std::mutex> lk(p->prof_mu);
-  p->prof_record = record;
-  p->prof_events.assign(events, events + 2 * n_pairs);
-  p->prof_count = 0;
+  if (n_pairs == 0) {
+    p->prof.erase(record);
+  } else {
+    auto& pr = p->prof[record];
+    pr.events.assign(events, events + 2 * n_pairs);
+    pr.count = 0;
+  }
   return CANVAS_OK;
 }
 
-int64_t canvas_plan_profile_count(const canvas_plan* p) { return p ? p->prof_count : -1; }
+int64_t canvas_plan_profile_count(const canvas_plan* p, int record) {
+  if (!p) return -1;
+  std::lock_guard<std::mutex> lk(p->prof_mu);
+  auto it = p->prof.find(record);
+  return it == p->prof.end() ? 0 : it->second.count;
+}
 
 int canvas_forward(const canvas_plan* p, int64_t batch, const float* x, const float* const* fc_w, int n_fc, float* y,
                    void* saved, void* workspace, void* stream) {

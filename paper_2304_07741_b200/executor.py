@@ -76,7 +76,7 @@ def load_library() -> ctypes.CDLL:
         lib.canvas_plan_launches.argtypes = [c.c_void_p, c.c_int]
         lib.canvas_forward.argtypes = [c.c_void_p, c.c_int64, c.c_void_p, c.c_void_p, c.c_int, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p]
         lib.canvas_plan_profile.argtypes = [c.c_void_p, c.c_int, c.c_void_p, c.c_int]
-        lib.canvas_plan_profile_count.argtypes = [c.c_void_p]
+        lib.canvas_plan_profile_count.argtypes = [c.c_void_p, c.c_int]
         lib.canvas_plan_profile_count.restype = c.c_int64
         lib.canvas_backward.argtypes = [c.c_void_p, c.c_int64, c.c_void_p, c.c_void_p, c.c_int, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p]
         _lib = lib
@@ -134,8 +134,8 @@ class DevicePlan:
             arr[2 * i + 1] = b.cuda_event
         _check(self.lib.canvas_plan_profile(self.handle, record, arr, len(events)))
 
-    def profile_count(self) -> int:
-        return self.lib.canvas_plan_profile_count(self.handle)
+    def profile_count(self, record: int) -> int:
+        return self.lib.canvas_plan_profile_count(self.handle, record)
 
     @staticmethod
     def _ptr_array(tensors) -> ctypes.Array:

@@ -90,7 +90,7 @@ def main():
         for _ in range(a.iters):
             step()
         torch.cuda.synchronize()
-        cnt = dp.profile_count()
+        cnt = dp.profile_count(i)
         dp.profile(i, [])
         ts = [u.elapsed_time(v) for u, v in evs[: min(cnt, len(evs))]]
         ms = statistics.median(ts)
