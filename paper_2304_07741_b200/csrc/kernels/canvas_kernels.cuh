@@ -186,6 +186,47 @@ __device__ __forceinline__ void gemm_wgrad(const CanvasArgs& a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// wgrad for FCs with few output channels (M <= 16, e.g. fc(G)): a tensor tile
+// would be >90% padding.  Each CTA stages 64-pixel tiles of both operands in
+// shared memory (coalesced along pixels) and each thread accumulates one or
+// more (m, j) outputs over its pixel chunk; partials are reduced in order.
+// grid = (ceil(J/JT), 1, chunks), JT = 256 / M rounded down to a power of 2.
+// ---------------------------------------------------------------------------
+template <class F>
+__device__ __forceinline__ void wgrad_small(const CanvasArgs& a) {
+  constexpr int TP = 64;
+  constexpr int JT = F::JT;
+  __shared__ float As[F::M][TP + 1];
+  __shared__ float Bs[JT][TP + 1];
+  const long long T = a.n * (long long)F::S;
+  const long long tbeg = (long long)blockIdx.z * F::TCHUNK;
+  const long long tend = tbeg + F::TCHUNK < T ? tbeg + F::TCHUNK : T;
+  const int j0 = blockIdx.x * JT;
+  const int tid = threadIdx.x;
+  const int om = tid / JT, oj = tid % JT;  // output owned by this thread (tid < M*JT)
+  float acc = 0.f;
+  for (long long t0 = tbeg; t0 < tend; t0 += TP) {
+    const int p = tid % TP;
+    const long long t = t0 + p;
+    const bool ok = t < tend;
+    const long long n = ok ? t / F::S : 0;
+    const int s = ok ? (int)(t - n * F::S) : 0;
+    for (int r = tid / TP; r < F::M; r += blockDim.x / TP) As[r][p] = ok ? F::A(a, n, r, s) : 0.f;
+    for (int r = tid / TP; r < JT; r += blockDim.x / TP) {
+      const int j = j0 + r;
+      Bs[r][p] = (ok && j < F::J) ? F::B(a, n, j, s) : 0.f;
+    }
+    __syncthreads();
+    if (om < F::M) {
+#pragma unroll 8
+      for (int q = 0; q < TP; ++q) acc = fmaf(As[om][q], Bs[oj][q], acc);
+    }
+    __syncthreads();
+  }
+  if (om < F::M && j0 + oj < F::J) F::partials(a)[((long long)blockIdx.z * F::M + om) * F::J + j0 + oj] = acc;
+}
+
 template <class F>
 __device__ __forceinline__ void reduce_partials(const CanvasArgs& a) {
   const long long T = a.n * (long long)F::S;

@@ -1066,8 +1066,9 @@ class Lowerer:
 
     def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops) -> None:
         """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
-        use_tc = self.use_tc and J >= 32
-        tchunk = TC_WGRAD_TCHUNK if use_tc else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
+        small = M <= 16
+        use_tc = self.use_tc and J >= 32 and not small
+        tchunk = TC_WGRAD_TCHUNK if (use_tc or small) else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
         self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
         fa, fb = Fn(self), Fn(self)
@@ -1098,6 +1099,14 @@ class Lowerer:
             k = self.add_kernel(name, functor, launcher)
             grid = (GridRule(0, J, 128), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
             self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+        elif small:
+            jt = 1 << max(0, (256 // M).bit_length() - 1)
+            jt = min(jt, 1 << (J - 1).bit_length()) if J > 1 else 1
+            functor = functor[: functor.rindex("};")] + f"  static constexpr int JT = {jt};\n}};\n"
+            launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::wgrad_small<{name}_F>(a); }}\n'
+            k = self.add_kernel(name, functor, launcher)
+            grid = (GridRule(0, J, jt), GridRule(0, 1, 1), GridRule(S, 0, tchunk))
+            self.p.launches.append(Launch("kernel", 1, name, k, 256, grid, tuple(fa.local_slots), BETA_NONE, what="small " + what, bytes_per_image=nbytes, flops_per_image=flops))
         else:
             launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_wgrad<{name}_F>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)

@@ -78,6 +78,9 @@ void gemm_wgrad(const CanvasArgs& a) {
 }
 
 template <class F>
+void wgrad_small(const CanvasArgs& a) { gemm_wgrad<F>(a); }
+
+template <class F>
 void reduce_partials(const CanvasArgs& a) {
   const long long T = a.n * (long long)F::S;
   const int Z = (int)((T + F::TCHUNK - 1) / F::TCHUNK);
