@@ -233,10 +233,22 @@ __device__ __forceinline__ void reduce_partials(const CanvasArgs& a) {
   const int Z = (int)((T + F::TCHUNK - 1) / F::TCHUNK);
   const float* __restrict__ P = a.p[0];
   float* __restrict__ out = a.p[1];
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < F::MJ; idx += gridDim.x * blockDim.x) {
+  if (F::MJ >= 4096) {  // enough outputs: one thread per output, z in order
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < F::MJ; idx += gridDim.x * blockDim.x) {
+      float s = 0.f;
+      for (int z = 0; z < Z; ++z) s += P[(long long)z * F::MJ + idx];
+      out[idx] = s;
+    }
+    return;
+  }
+  // few outputs: one warp per output, lane-strided z then a fixed shuffle tree
+  const int lane = threadIdx.x & 31;
+  for (int idx = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; idx < F::MJ; idx += (gridDim.x * blockDim.x) >> 5) {
     float s = 0.f;
-    for (int z = 0; z < Z; ++z) s += P[(long long)z * F::MJ + idx];
-    out[idx] = s;
+    for (int z = lane; z < Z; z += 32) s += P[(long long)z * F::MJ + idx];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[idx] = s;
   }
 }
 

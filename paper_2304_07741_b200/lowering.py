@@ -1068,7 +1068,11 @@ class Lowerer:
         """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
         small = M <= 16
         use_tc = self.use_tc and J >= 32 and not small
-        tchunk = TC_WGRAD_TCHUNK if (use_tc or small) else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
+        if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
+            jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()))
+            tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
+        else:
+            tchunk = TC_WGRAD_TCHUNK if use_tc else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
         self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
         fa, fb = Fn(self), Fn(self)
@@ -1119,7 +1123,7 @@ class Lowerer:
             f'extern "C" __global__ void __launch_bounds__(256) {rname}(const CanvasArgs a) {{ canvas::reduce_partials<{rname}_F>(a); }}\n'
         )
         k2 = self.add_kernel(rname, "", rsrc)
-        grid2 = (GridRule(0, M * J, 256), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        grid2 = (GridRule(0, M * J * (1 if M * J >= 4096 else 32), 256), GridRule(0, 1, 1), GridRule(0, 1, 1))
         self.p.launches.append(Launch("kernel", 1, rname, k2, 256, grid2, (-1 - k_ws, dw_slot), BETA_NONE, what=f"wgrad reduce {M}x{J}"))
 
     # ---- backward

@@ -104,3 +104,13 @@ def test_candidate_evaluator_real_worker():
     res = CandidateEvaluator([0], shapes={"batch": 2, "h": 16, "w": 16, "c_in": 16, "c_out": 16}).run(texts, timeout_s=600)
     assert [r.status for r in res] == ["ok"] * 3, [r.error for r in res]
     assert all(r.fwd_ms > 0 and r.bwd_ms > 0 for r in res)
+
+
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+@pytest.mark.parametrize("cin,cout,hw,stride", [(256, 512, 14, 2), (512, 512, 7, 1), (128, 256, 28, 2)])
+def test_wide_channels(name, cin, cout, hw, stride):
+    """ResNet-18 stage-3/4 widths: multi-tile N (dgrad N = 9C split over tiles),
+    persistent and 16-producer-warp GEMM variants, packed weight images > 1 tile."""
+    case = reference(zoo.ALL[name], cin, cout, hw, hw, stride=stride, n=2)
+    y, dx, dws = run_gpu(case)
+    assert_close(case, y, dx, dws, f"{name} {cin}->{cout} {hw}^2 s{stride}")
