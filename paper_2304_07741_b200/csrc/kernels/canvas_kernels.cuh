@@ -309,13 +309,17 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// split x into (hi, lo): hi keeps the 10 explicit tf32 mantissa bits (mask),
-// lo = x - hi is exact in fp32 and is itself read as tf32 by the tensor core.
-// hi*hi + hi*lo + lo*hi then carries ~2^-20 relative error per product — the
-// 3xTF32 scheme at 2 instructions instead of two cvt.rna emulations.
+// split x into (hi, lo) tf32 values, both rounded to nearest on the 13 dropped
+// mantissa bits with an integer add + mask (finite inputs; carries into the
+// exponent round correctly): hi*hi + hi*lo + lo*hi then carries ~2^-22
+// relative error per product, the 3xTF32 accuracy, at 5 instructions instead
+// of two emulated cvt.rna.tf32.f32.
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xffffe000u);
-  lo = x - hi;
+  hi = tf32_rn(x);
+  lo = tf32_rn(x - hi);
 }
 
 __device__ __forceinline__ void st_shared_v4(void* p, float a, float b, float c, float d) {
@@ -436,11 +440,18 @@ struct Smem {
 };
 
 // MMA issuer: consumes STAGES-deep ring, 3 MMAs per K=8 step (hi.hi, hi.lo, lo.hi)
-template <int NT, int STAGES, bool A_MN = false>
+// NACC > 1: the K loop is split into NACC contiguous chunks accumulated in
+// separate TMEM regions (tmem + i*NT) and summed by the epilogue in fp32: the
+// tensor core's accumulation error grows with the accumulated length, and
+// chunking keeps K = 9C = 4608 (ResNet stage 4) inside the fp32 tolerance.
+template <int NT, int STAGES, bool A_MN = false, int NACC = 1>
 __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* empty, cv_u64* done, cv_u32 tmem, int KB) {
   using L = Smem<NT, STAGES>;
   constexpr cv_u32 idesc = idesc_tf32(NT, A_MN);
   for (int kb = 0; kb < KB; ++kb) {
+    const int acc = (kb * NACC) / KB;
+    const bool fresh = kb == 0 || ((kb - 1) * NACC) / KB != acc;
+    const cv_u32 d = tmem + acc * NT;
     const int st = kb % STAGES;
     mbar_wait(&full[st], (kb / STAGES) & 1);
     fence_after();
@@ -459,9 +470,9 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
         dah = desc_k_sw128(a_hi + o);
         dal = desc_k_sw128(a_lo + o);
       }
-      mma_tf32(tmem, dah, desc_k_sw128(b_hi + o), idesc, (kb | kk) != 0);
-      mma_tf32(tmem, dah, desc_k_sw128(b_lo + o), idesc, 1);
-      mma_tf32(tmem, dal, desc_k_sw128(b_hi + o), idesc, 1);
+      mma_tf32(d, dah, desc_k_sw128(b_hi + o), idesc, !(fresh && kk == 0));
+      mma_tf32(d, dah, desc_k_sw128(b_lo + o), idesc, 1);
+      mma_tf32(d, dal, desc_k_sw128(b_hi + o), idesc, 1);
     }
     commit(&empty[st]);
   }
@@ -475,13 +486,13 @@ __device__ __forceinline__ void mma_loop(uint8_t* smem, cv_u64* full, cv_u64* em
 // MMA rows = 128 pixels t = n*S + s (operand B(n,k,s), computed), MMA cols =
 // NT output channels (operand A(m,k), weights).
 // ---------------------------------------------------------------------------
-template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = tc::kProducerWarps>
+template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = tc::kProducerWarps, int NACC = 1>
 __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   static_assert(A_MN || PW == tc::kProducerWarps, "K-major producer mapping assumes 8 warps");
   static_assert(32 % PW == 0 && PW % 4 == 0, "PW must divide the k-block and cover the TMEM quadrants");
   using namespace tc;
   using L = Smem<NT, STAGES>;
-  constexpr int NCOLS = TmemCols<NT>::value;
+  constexpr int NCOLS = TmemCols<NT * NACC>::value;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((unsigned long long)smem_raw + 1023) & ~1023ull);
   cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
@@ -644,6 +655,13 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
     for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {
       float v[16];
       tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + cc, v);
+#pragma unroll
+      for (int c2 = 1; c2 < NACC; ++c2) {
+        float u[16];
+        tmem_ld16(tmem + c2 * NT + ((cv_u32)(q * 32) << 16) + cc, u);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += u[j];
+      }
       if (eok) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -653,7 +671,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       }
     }
   } else if (warp == PW) {
-    if (lane == 0) mma_loop<NT, STAGES, A_MN>(smem, full, empty, done, tmem, KB);
+    if (lane == 0) mma_loop<NT, STAGES, A_MN, NACC>(smem, full, empty, done, tmem, KB);
   } else if (PACKED && lane == 0) {
     // B operand: pre-split, pre-swizzled weight tile images (tc_pack_b), one
     // TMA bulk copy of {hi, lo} per k-block

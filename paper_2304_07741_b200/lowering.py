@@ -63,14 +63,15 @@ TC_NTMAX = int(os.environ.get("CANVAS_TC_NTMAX", "256"))  # widest MMA N tile
 TC_PERSIST = os.environ.get("CANVAS_TC_PERSIST", "1") == "1"  # persistent fwd/dgrad GEMMs
 TC_PW = int(os.environ.get("CANVAS_TC_PW", "8"))  # producer warps of the persistent GEMM
 SMS = 148
+TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 TC_WGRAD_TCHUNK = 4096
 TC_WGRAD_PW = int(os.environ.get("CANVAS_WGRAD_PW", "16"))  # wgrad producer warps
 TC_PIX_PW = int(os.environ.get("CANVAS_PIX_PW", "0"))  # 0 = auto  # fwd/dgrad (non-persistent) producer warps  # pixels per wgrad split (128 k-blocks of 32)
 
 
-def tc_tile(cols: int) -> tuple[int, int, int]:
+def tc_tile(cols: int, ntmax: int | None = None) -> tuple[int, int, int]:
     """(NT, number of column tiles, pipeline stages) for an MMA N extent of ``cols``."""
-    nct = -(-cols // TC_NTMAX)
+    nct = -(-cols // (ntmax or TC_NTMAX))
     nt = -(-(-(-cols // nct)) // 16) * 16
     stage = 2 * 128 * 128 + 2 * nt * 128
     if 2 * stage + 2048 <= TC_SMEM_PAIR:
@@ -1018,7 +1019,12 @@ class Lowerer:
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }", "};"]
         functor = "\n".join(lines) + "\n"
         if self.use_tc and M >= 8 and K >= 16:
-            nt, nct, stages = tc_tile(M)
+            # long reductions run over NACC TMEM accumulators (<= TC_ACC_K terms each),
+            # which caps the column tile so NACC x NT fits the 512 TMEM columns
+            nacc = 1
+            while nacc < 4 and K > TC_ACC_K * nacc:
+                nacc *= 2
+            nt, nct, stages = tc_tile(M, min(TC_NTMAX, 512 // nacc))
             smem = tc_smem_bytes(nt, stages)
             kb = -(-K // 32)
             pack_bytes = nct * kb * 2 * nt * 128
@@ -1050,8 +1056,8 @@ class Lowerer:
             if pw > 8:
                 stages = max(2, min(4, (220 * 1024) // (2 * 128 * 128 + 2 * nt * 128)))
                 smem = tc_smem_bytes(nt, stages)
-            pair = smem <= TC_SMEM_PAIR and pw <= 8
-            launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true, {TC_A_MN}, {pw}>(a); }}\n'
+            pair = smem <= TC_SMEM_PAIR and pw <= 8 and 2 * nt * nacc <= 512
+            launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix<{name}_F, {nt}, {stages}, true, {TC_A_MN}, {pw}, {nacc}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
             total = nct * kb * nt * 32

@@ -90,7 +90,7 @@ void reduce_partials(const CanvasArgs& a) {
     a.p[1][idx] = s;
   }
 }
-template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = 8>
+template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = 8, int NACC = 1>
 void tc_gemm_pix(const CanvasArgs& a) { gemm_nk<F>(a); }
 template <class F, int NT>
 void tc_pack_b(const CanvasArgs&) {}
