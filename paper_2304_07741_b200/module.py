@@ -113,20 +113,80 @@ class CanvasConv2d(nn.Module):
         return f"{self.in_channels}, {self.out_channels}, k={self.kernel_size}, stride={self.stride}, copies={self.copies}, fc={self.fc_shapes}"
 
 
-def replace(model: nn.Module, ir_text: str, *, g: int = 4, xs: dict | None = None, kernel_sizes=(3,), factory=None) -> list[str]:
+def replace(model: nn.Module, ir_text: str, *, g: int = 4, xs: dict | None = None, xs_by_name: dict | None = None, kernel_sizes=(3,), factory=None) -> list[str]:
     """Swap every eligible ``nn.Conv2d`` (kernel size in ``kernel_sizes``) for a Canvas module.
 
-    ``factory(conv) -> nn.Module`` overrides the replacement (the CPU
-    reference path uses it with oracle modules).  Returns the replaced names.
+    ``xs_by_name`` gives per-target free-variable values (a level-2
+    ``Solution``, see ``solve_for_model``); ``factory(conv) -> nn.Module``
+    overrides the replacement (the CPU reference path uses it with oracle
+    modules).  Returns the replaced names.
     """
     done = []
     for name, parent in list(model.named_modules()):
         for cname, child in list(parent.named_children()):
             if conv_is_target(child) and child.kernel_size[0] in kernel_sizes:
+                full = f"{name}.{cname}" if name else cname
+                txs = (xs_by_name or {}).get(full, xs)
                 if factory is not None:
                     new = factory(child)
                 else:
-                    new = CanvasConv2d(ir_text, child.in_channels, child.out_channels, child.kernel_size[0], child.stride[0], g=g, xs=xs, bias=child.bias is not None)
+                    new = CanvasConv2d(ir_text, child.in_channels, child.out_channels, child.kernel_size[0], child.stride[0], g=g, xs=txs, bias=child.bias is not None)
                 setattr(parent, cname, new)
                 done.append(f"{name}.{cname}" if name else cname)
     return done
+
+
+def backbone_spec(model: nn.Module, input_shape=(1, 3, 224, 224), kernel_sizes=(3,)):
+    """SPEC.md:376-381 BackboneSpec of a torch model: replacement targets with
+    their output resolution (traced with forward hooks on a CPU copy of one
+    image) and the analytical cost of everything that stays (other convs,
+    linears: MACs and weights; BN: 2 params per channel)."""
+    import copy
+
+    from .canvas.constraint_solver import BackboneSpec, Target
+
+    m = copy.deepcopy(model).cpu().eval()
+    shapes: dict = {}
+    hooks = []
+    for name, mod in m.named_modules():
+        if isinstance(mod, (nn.Conv2d, nn.Linear)):
+            hooks.append(mod.register_forward_hook(lambda mod_, i, o, name=name: shapes.__setitem__(name, tuple(o.shape))))
+    with torch.no_grad():
+        m(torch.zeros(input_shape))
+    for h in hooks:
+        h.remove()
+    targets, nf, npar = [], 0, 0
+    for name, mod in m.named_modules():
+        if isinstance(mod, nn.Conv2d):
+            kh, kw = mod.kernel_size
+            ho, wo = shapes[name][2:]
+            params = mod.in_channels * mod.out_channels * kh * kw // mod.groups
+            flops = params * ho * wo
+            if conv_is_target(mod) and kh in kernel_sizes:
+                targets.append(Target(name, mod.in_channels, mod.out_channels, ho, wo, kh, kw, flops, params))
+            else:
+                nf += flops
+                npar += params + (mod.out_channels if mod.bias is not None else 0)
+        elif isinstance(mod, nn.Linear):
+            nf += mod.in_features * mod.out_features
+            npar += mod.in_features * mod.out_features + (mod.out_features if mod.bias is not None else 0)
+        elif isinstance(mod, nn.BatchNorm2d):
+            npar += 2 * mod.num_features
+    return BackboneSpec(tuple(targets), nf, npar)
+
+
+def solve_for_model(model: nn.Module, ir_text: str, *, flops_frac: float | None = None, params_frac: float | None = None, g: int | None = None, input_shape=(1, 3, 224, 224)):
+    """The paper's ``canvas.sample(nn, budget)`` solve step (§6.3):
+    level-2 solve of one kernel over a network under a budget given as a
+    fraction of the original totals.  Returns (Solution | None, spec, xs_by_name)."""
+    from .canvas import ir as cir
+    from .canvas.constraint_solver import Budget, solve_network
+    from .canvas.cost_model import original_cost
+
+    spec = backbone_spec(model, input_shape)
+    of, op = original_cost(spec)
+    budget = Budget(int(of * flops_frac) if flops_frac is not None else None, int(op * params_frac) if params_frac is not None else None)
+    tmpl = cir.parse(ir_text).template
+    sol = solve_network(tmpl, spec, budget, g=g)
+    xs_by_name = {t.name: sol.target_xs(i) for i, t in enumerate(spec.targets)} if sol else {}
+    return sol, spec, xs_by_name
