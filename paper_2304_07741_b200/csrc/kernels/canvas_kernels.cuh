@@ -499,9 +499,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   cv_u64* empty = full + STAGES;
   cv_u64* done = empty + STAGES;
   cv_u32* tslot = (cv_u32*)(done + 1);
-  // warp index through a shuffle: provably warp-uniform, so the channel index math of
-  // the functors (k or row decomposition) runs on the uniform datapath
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int KB = (F::K + kBK - 1) / kBK;
 
   if (threadIdx.x == 0) {
@@ -728,9 +726,7 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
   cv_u64* tfull = empty + STAGES;   // [2]
   cv_u64* tempty = tfull + 2;       // [2]
   cv_u32* tslot = (cv_u32*)(tempty + 2);
-  // warp index through a shuffle: provably warp-uniform, so the channel index math of
-  // the functors (k or row decomposition) runs on the uniform datapath
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long T = a.n * (long long)F::S;
   const long long PT = (T + kBM - 1) / kBM;
   const long long TILES = PT * NCT;
@@ -937,9 +933,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   cv_u64* empty = full + STAGES;
   cv_u64* done = empty + STAGES;
   cv_u32* tslot = (cv_u32*)(done + 1);
-  // warp index through a shuffle: provably warp-uniform, so the channel index math of
-  // the functors (k or row decomposition) runs on the uniform datapath
-  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
