@@ -60,6 +60,81 @@ __device__ __forceinline__ void pointwise(const CanvasArgs& a) {
 }
 
 // ---------------------------------------------------------------------------
+// K2: softmax / row-dot over a channel span with SL threads per row.  When
+// rows are few and long (ResNet stage 4: 49 pixels x 512 channels) a thread
+// per row starves the GPU; here RPB = 256/SL rows per CTA, each row's span is
+// split across SL threads (rows innermost: loads stay coalesced along pixels)
+// and the partial max / sum / dot are combined in shared memory in a fixed
+// order (deterministic).  F::in(a,n,r,j), F::out(a,n,r,j,y) (softmax) or
+// F::term(a,n,r,j), F::put(a,n,r,v) (row-dot); F::ROWS rows of F::SPAN.
+// ---------------------------------------------------------------------------
+template <class F, int SL>
+__device__ __forceinline__ void softmax_rows(const CanvasArgs& a) {
+  constexpr int RPB = 256 / SL;
+  __shared__ float red[SL][RPB + 1];
+  const long long total = a.n * F::ROWS;
+  const int tr = threadIdx.x % RPB, sl = threadIdx.x / RPB;
+  for (long long rb = (long long)blockIdx.x * RPB; rb < total; rb += (long long)gridDim.x * RPB) {
+    const long long row = rb + tr;
+    const bool ok = row < total;
+    const long long n = ok ? row / F::ROWS : 0;
+    const int r = ok ? (int)(row - n * F::ROWS) : 0;
+    float m = -INFINITY, s = 0.f;
+    if (ok) {
+      for (int j = sl; j < F::SPAN; j += SL) {
+        const float x = F::in(a, n, r, j);
+        if (x > m) {
+          s = s * expf(m - x) + 1.f;
+          m = x;
+        } else {
+          s += expf(x - m);
+        }
+      }
+    }
+    red[sl][tr] = m;
+    __syncthreads();
+    float M = red[0][tr];
+#pragma unroll
+    for (int i = 1; i < SL; ++i) M = fmaxf(M, red[i][tr]);
+    __syncthreads();
+    red[sl][tr] = m == -INFINITY ? 0.f : s * expf(m - M);
+    __syncthreads();
+    float S = 0.f;
+#pragma unroll
+    for (int i = 0; i < SL; ++i) S += red[i][tr];
+    __syncthreads();
+    if (ok)
+      for (int j = sl; j < F::SPAN; j += SL) F::out(a, n, r, j, expf(F::in(a, n, r, j) - M) / S);
+  }
+}
+
+template <class F, int SL>
+__device__ __forceinline__ void rowdot_rows(const CanvasArgs& a) {
+  constexpr int RPB = 256 / SL;
+  __shared__ float red[SL][RPB + 1];
+  const long long total = a.n * F::ROWS;
+  const int tr = threadIdx.x % RPB, sl = threadIdx.x / RPB;
+  for (long long rb = (long long)blockIdx.x * RPB; rb < total; rb += (long long)gridDim.x * RPB) {
+    const long long row = rb + tr;
+    const bool ok = row < total;
+    const long long n = ok ? row / F::ROWS : 0;
+    const int r = ok ? (int)(row - n * F::ROWS) : 0;
+    float acc = 0.f;
+    if (ok)
+      for (int j = sl; j < F::SPAN; j += SL) acc += F::term(a, n, r, j);
+    red[sl][tr] = acc;
+    __syncthreads();
+    if (sl == 0 && ok) {
+      float d = 0.f;
+#pragma unroll
+      for (int i = 0; i < SL; ++i) d += red[i][tr];
+      F::put(a, n, r, d);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3 (SIMT): FC forward / dgrad.  Rows t = n*S + s are flattened so small
 // spatial extents (7x7) still fill 64-wide tiles.  B is evaluated by the
 // functor (fused producer chain), staged through shared memory once per tile.

@@ -860,7 +860,11 @@ class Lowerer:
                 pre, span, post = self.softmax_geom(nd)
                 rows = math.prod(pre) * math.prod(post)
                 rext = pre + post
-                self.launch_pointwise(name, rows, lambda f, v=v, tg=tg: self.body_softmax(f, v, tg), 0, beta, f"softmax -> n{v}", io, 0, inner=rext[-1] if rext else 1)
+                sl = self.row_split(rows, math.prod(span))
+                if sl > 1:
+                    self.launch_softmax_split(name, v, tg, sl, beta, io)
+                else:
+                    self.launch_pointwise(name, rows, lambda f, v=v, tg=tg: self.body_softmax(f, v, tg), 0, beta, f"softmax -> n{v}", io, 0, inner=rext[-1] if rext else 1)
             elif nd.op == "fc":
                 self.lower_fc_fwd(name, v, tg, beta)
             else:
@@ -942,6 +946,54 @@ class Lowerer:
                 f.store(d, c, y, beta)
 
         loop(write)
+
+    @staticmethod
+    def row_split(rows: int, span: int) -> int:
+        """Threads per softmax row: enough rows x slices to fill the GPU at batch 256."""
+        want = -(-(SMS * 2048) // (256 * rows))
+        sl = 1
+        while sl < want and sl < 32 and sl * 2 <= span:
+            sl *= 2
+        return sl
+
+    def _row_functor(self, name: str, nd, methods) -> tuple[str, list]:
+        """Functor with ROWS/SPAN and one static method per (signature, body_fn)."""
+        pre, span, post = self.softmax_geom(nd)
+        slots: list = []
+        lines = [f"struct {name}_F {{", f"  static constexpr long long ROWS = {math.prod(pre) * math.prod(post)}LL;", f"  static constexpr int SPAN = {math.prod(span)};"]
+        for sig, body in methods:
+            f = Fn(self)
+            f.pre = []
+            f.computing = None
+            f.local_slots = slots
+            rc = f.decompose("r", pre + post)
+            pc, qc = tuple(rc[: len(pre)]), tuple(rc[len(pre) :])
+            sc = tuple(f.decompose("j", span)) if "int j" in sig else ()
+            ret = body(f, pc + sc + qc, pc + qc)
+            lines.append(f"  static __device__ __forceinline__ {sig} {{")
+            lines += ["    " + x for x in f.pre] + f.lines
+            if ret is not None:
+                lines.append(f"    return {ret};")
+            lines.append("  }")
+        lines.append("};")
+        return "\n".join(lines) + "\n", slots
+
+    def launch_softmax_split(self, name, v, targets, sl, beta, io) -> None:
+        nd = self.nodes[v]
+
+        def out(f, c, rowc):
+            for d, b in targets:
+                f.store(d, c, "y", b)
+
+        functor, slots = self._row_functor(name, nd, [
+            ("float in(const CanvasArgs& a, const long long n, const int r, const int j)", lambda f, c, rowc: self.val(f, nd.ins[0], c)),
+            ("void out(const CanvasArgs& a, const long long n, const int r, const int j, const float y)", out),
+        ])
+        launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::softmax_rows<{name}_F, {sl}>(a); }}\n'
+        k = self.add_kernel(name, functor, launcher)
+        rows = math.prod(self.softmax_geom(nd)[0]) * math.prod(self.softmax_geom(nd)[2])
+        grid = (GridRule(rows, 0, 256 // sl, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        self.p.launches.append(Launch("kernel", 0, name, k, 256, grid, tuple(slots), beta, what=f"softmax -> n{v} ({sl} threads/row)", bytes_per_image=io))
 
     # ---- FC
     def fc_weight_slot(self, u: int) -> tuple[int, int]:
@@ -1078,7 +1130,12 @@ class Lowerer:
             jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()))
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
         else:
-            tchunk = TC_WGRAD_TCHUNK if use_tc else max(2048, -(-4096 * S // 60000) * GEMM_TILE)
+            if use_tc:  # >= ~6 CTAs per SM at batch 256 without going below 512 pixels per partial
+                tiles = -(-J // 128) * tc_tile(M)[1]
+                z = -(-(6 * SMS) // tiles)
+                tchunk = min(TC_WGRAD_TCHUNK, max(512, -(-(-(-(256 * S) // z)) // 128) * 128))
+            else:
+                tchunk = max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
         self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
         fa, fb = Fn(self), Fn(self)
@@ -1217,6 +1274,24 @@ class Lowerer:
 
         name = f"k{len(self.p.kernel_names)}_bwd_softmaxdot{u}"
         rext = pre + post
+        sl = self.row_split(rows, S)
+        if sl > 1:
+
+            def term(f, c, rowc):
+                return f.fvar(f"{self.grad(f, u, c)} * {self.val(f, u, c)}")
+
+            def put(f, c, rowc):
+                f.store(d, rowc, "v", False)
+
+            functor, slots = self._row_functor(name, nu, [
+                ("float term(const CanvasArgs& a, const long long n, const int r, const int j)", term),
+                ("void put(const CanvasArgs& a, const long long n, const int r, const float v)", put),
+            ])
+            launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::rowdot_rows<{name}_F, {sl}>(a); }}\n'
+            k = self.add_kernel(name, functor, launcher)
+            grid = (GridRule(rows, 0, 256 // sl, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+            self.p.launches.append(Launch("kernel", 1, name, k, 256, grid, tuple(slots), BETA_NONE, what=f"softmax row-dot n{u} ({sl} threads/row)", bytes_per_image=4 * (2 * nu.numel + rows)))
+            return
         self.launch_pointwise(name, rows, body, 1, BETA_NONE, f"softmax row-dot n{u}", 4 * (2 * nu.numel + rows), 0, inner=rext[-1] if rext else 1)
 
     def lower_fc_bwd(self, u: int, dx_beta: int) -> None:

@@ -80,6 +80,27 @@ void gemm_wgrad(const CanvasArgs& a) {
 template <class F>
 void wgrad_small(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 
+template <class F, int SL>
+void softmax_rows(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int r = 0; r < (int)F::ROWS; ++r) {
+      float m = -INFINITY, s = 0.f;
+      for (int j = 0; j < F::SPAN; ++j) m = std::max(m, F::in(a, n, r, j));
+      for (int j = 0; j < F::SPAN; ++j) s += std::exp(F::in(a, n, r, j) - m);
+      for (int j = 0; j < F::SPAN; ++j) F::out(a, n, r, j, std::exp(F::in(a, n, r, j) - m) / s);
+    }
+}
+
+template <class F, int SL>
+void rowdot_rows(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int r = 0; r < (int)F::ROWS; ++r) {
+      float d = 0.f;
+      for (int j = 0; j < F::SPAN; ++j) d += F::term(a, n, r, j);
+      F::put(a, n, r, d);
+    }
+}
+
 template <class F>
 void reduce_partials(const CanvasArgs& a) {
   const long long T = a.n * (long long)F::S;
