@@ -52,7 +52,7 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
 
 
-def build_model(kernel: str, device=None, cpu_reference: bool = False):
+def build_model(kernel: str, device=None, cpu_reference: bool = False, fuse_bn: bool = True):
     import torchvision
 
     from paper_2304_07741_b200.module import replace
@@ -69,6 +69,10 @@ def build_model(kernel: str, device=None, cpu_reference: bool = False):
         names = replace(m, text, factory=factory)
     else:
         names = replace(m, text, g=4)
+        if fuse_bn:
+            from paper_2304_07741_b200.post import fuse_backbone
+
+            assert fuse_backbone(m) == 20  # BN post-pass (+ReLU, +residual) on libcanvas_post
     assert len(names) == 16, names
     return m.to(device) if device is not None else m
 
@@ -190,6 +194,7 @@ def main() -> None:
     ap.add_argument("--ref-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-context", action="store_true")
+    ap.add_argument("--no-fuse-bn", action="store_true", help="keep the backbone's cuDNN BatchNorm2d + ReLU")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "canvas" else args.warmup
 
@@ -207,7 +212,7 @@ def main() -> None:
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.benchmark = True
 
-    model = build_model(args.kernel, dev)
+    model = build_model(args.kernel, dev, fuse_bn=not args.no_fuse_bn)
     if world > 1:
         from torch.nn.parallel import DistributedDataParallel as DDP
 
@@ -254,6 +259,9 @@ def main() -> None:
         if isinstance(m, CanvasConv2d):
             for p in m._plans.values():
                 per_step_launches += p.launches(0) + p.launches(1)
+    from paper_2304_07741_b200.post import FusedBatchNorm2d
+
+    per_step_launches += 4 * sum(isinstance(m, FusedBatchNorm2d) for m in core.modules())  # stats+apply, reduce+apply
 
     clocks = Clocks(local)
     if world > 1:

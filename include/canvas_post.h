@@ -1,0 +1,63 @@
+/*
+ * canvas_post.h — C ABI of the post-pass of a replaced conv
+ * (libcanvas_post.so): training-mode BatchNorm2d over the Canvas kernel's
+ * output with the block's ReLU and residual add fused in.
+ *
+ * What it replaces in the reference:
+ *   SPEC.md:658 (trainer_plugin.build_module, "BN post-pass" after the FC of
+ *   a built module) and, in the network path, the
+ *   backbone BatchNorm2d that follows every replaced nn.Conv2d; the reference
+ *   specifies both but ships no numeric code.
+ *   Semantics are torch.nn.functional.batch_norm(training=True) followed by
+ *   (+ residual) and ReLU: biased variance for normalisation, unbiased for the
+ *   running variance, running = (1 - momentum) * running + momentum * batch.
+ *
+ * Conventions: fp32, contiguous [N, C, H*W] device tensors owned by the
+ * caller; `workspace` holds canvas_bn_workspace() bytes of per-slice
+ * partials; calls only enqueue kernels on `stream` (no allocation, no sync;
+ * CUDA-graph capturable).  Deterministic: no atomics.  0 = OK, negative =
+ * error (message from canvas_post_last_error, thread-local).
+ */
+#ifndef CANVAS_POST_H
+#define CANVAS_POST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CANVAS_POST_ABI_VERSION 1
+#define CANVAS_POST_OK 0
+#define CANVAS_POST_ERR_ARGS (-5)
+#define CANVAS_POST_ERR_CUDA (-4)
+
+int canvas_post_abi_version(void);
+
+/* Bytes of workspace a BN forward or backward call at this shape needs. */
+size_t canvas_bn_workspace(int64_t N, int64_t C, int64_t HW);
+
+/* y = act(bn(x) [+ residual]); act = ReLU when relu != 0.  running_mean /
+ * running_var may both be NULL (no running-stat update).  Writes the batch
+ * mean and 1/sqrt(var + eps) to save_mean / save_invstd for the backward. */
+int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const float* residual, float* y,
+                      const float* gamma, const float* beta, float* running_mean, float* running_var,
+                      float* save_mean, float* save_invstd, float momentum, float eps, int relu, void* workspace,
+                      void* stream);
+
+/* dx (and dresidual = the gradient reaching the residual, when non-NULL),
+ * dgamma, dbeta (written, not accumulated) from dy = dL/dy.  y is the
+ * forward output, used as the ReLU mask (relu'(0) = 0); may be NULL when
+ * relu == 0. */
+int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const float* dy,
+                       const float* gamma, const float* save_mean, const float* save_invstd, float* dx,
+                       float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace, void* stream);
+
+const char* canvas_post_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CANVAS_POST_H */

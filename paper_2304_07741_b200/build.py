@@ -4,6 +4,8 @@
    as a string into ``libcanvas_b200.so`` so NVRTC can instantiate it per plan.
 2. ``libcanvas_b200.so`` (C ABI, include/canvas_b200.h) is built with g++; it
    dlopens the CUDA driver and NVRTC at first use.
+   ``libcanvas_post.so`` (include/canvas_post.h, the fused BN post-pass) is
+   compiled by nvcc for sm_100a from ``csrc/post_kernels.cu``.
 3. Build check: the pinned kernels (zoo.py) are lowered and their generated
    functors compiled together with the templates by ``nvcc`` for sm_100a
    (``-gencode arch=compute_100a,code=sm_100a -lineinfo``) into
@@ -23,6 +25,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libcanvas_b200.so"
+POST_LIB = PKG / "libcanvas_post.so"
 BUILD = ROOT / "build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -58,6 +61,18 @@ def build_lib() -> Path:
     return LIB
 
 
+def build_post() -> Path:
+    """libcanvas_post.so: BN post-pass kernels (include/canvas_post.h), nvcc for sm_100a."""
+    src = CSRC / "post_kernels.cu"
+    hdr = ROOT / "include" / "canvas_post.h"
+    if POST_LIB.exists() and POST_LIB.stat().st_mtime >= max(src.stat().st_mtime, hdr.stat().st_mtime):
+        return POST_LIB
+    tmp = POST_LIB.with_suffix(".so.tmp")
+    _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-I", str(ROOT / "include"), str(src), "-o", str(tmp)])
+    tmp.replace(POST_LIB)
+    return POST_LIB
+
+
 def pinned_source() -> str:
     """Generated functors of every pinned kernel at config-1 shapes, one file."""
     from . import zoo
@@ -90,6 +105,7 @@ def build_check(verbose: bool = False) -> Path:
 
 def build(verbose: bool = False) -> None:
     build_lib()
+    build_post()
     build_check(verbose)
 
 

@@ -1,0 +1,383 @@
+// Post-pass kernels of a replaced conv: training-mode BatchNorm2d with the
+// activation (ReLU) and the residual add of the enclosing block fused in.
+//
+// SPEC.md:658 specifies a BN post-pass for `build_module`; SURVEY App. A.10
+// keeps the backbone's own BN after every replaced conv.  Both are the same
+// operation on the replaced conv's output, [N, C, H, W] fp32 (App. A.0), and
+// it is a pure HBM-bound pass: per channel c over M = N*H*W elements
+//
+//   forward   mean, var (biased) -> y = act((x - mean) * invstd * gamma + beta [+ r])
+//   backward  g = dy * [y > 0]; Sg = sum g; Sgx = sum g * xhat
+//             dx = gamma * invstd * (g - Sg / M - xhat * Sgx / M); dr = g
+//
+// which are torch.nn.functional.batch_norm (training) semantics, including
+// the running-stat update (unbiased variance, momentum) and relu'(0) = 0
+// (App. A.5, taken on the output like torch's threshold_backward).
+//
+// Layout of the work: channel c is split into P slices of whole images; one
+// 256-thread CTA per (slice, channel), C*P ~ 8 CTAs per SM.  Inside a slice
+// a CTA streams image planes with 16-byte loads when H*W % 4 == 0, and packs
+// several small planes (7x7, 14x14) into one pass of the CTA so every thread
+// stays busy.  Reductions are deterministic: per-thread fp32 sums of
+// mean-shifted values (shift = x[0, c, 0, 0]), a fixed-order warp/CTA tree in
+// fp64, per-slice partials in a workspace, and a fixed-order sum of the P
+// partials by every consumer CTA.  No atomics: identical inputs give
+// identical bits.
+//
+// Launches: forward = stats + apply, backward = reduce + apply (4 per BN).
+
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdint.h>
+
+#include "canvas_post.h"
+
+namespace {
+
+constexpr int kBlock = 256;
+
+struct Geo {
+  int N, C, HW, P, V, U;  // V = vector width (4 or 1), U = HW / V units per plane
+};
+
+__host__ Geo make_geo(int N, int C, int HW, int P) {
+  Geo g{N, C, HW, P, 1, HW};
+  if (HW % 4 == 0) {
+    g.V = 4;
+    g.U = HW / 4;
+  }
+  return g;
+}
+
+// Calls f(offset_in_elements, vector_index_unused) for every V-wide unit of
+// channel c in slice p, each unit exactly once per CTA, in a fixed
+// thread -> unit mapping.
+template <int V, class Fn>
+__device__ __forceinline__ void for_units(const Geo& g, int c, int p, Fn&& f) {
+  const int n0 = (int)((long long)p * g.N / g.P);
+  const int n1 = (int)((long long)(p + 1) * g.N / g.P);
+  const long long plane = (long long)g.C * g.HW;
+  if (g.U >= kBlock) {
+    for (int n = n0; n < n1; ++n) {
+      const long long base = (long long)n * plane + (long long)c * g.HW;
+      for (int u = threadIdx.x; u < g.U; u += kBlock) f(base + (long long)u * V);
+    }
+  } else {
+    const int ipb = kBlock / g.U;
+    const int u = threadIdx.x % g.U;
+    const int j = threadIdx.x / g.U;
+    if (j < ipb)
+      for (int n = n0 + j; n < n1; n += ipb) f((long long)n * plane + (long long)c * g.HW + (long long)u * V);
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fixed-order CTA sum of two values; result valid in thread 0
+__device__ __forceinline__ void block_sum2(double& a, double& b) {
+  __shared__ double sa[kBlock / 32], sb[kBlock / 32];
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sa[w] = a;
+    sb[w] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a = 0.0;
+    b = 0.0;
+    for (int i = 0; i < kBlock / 32; ++i) {
+      a += sa[i];
+      b += sb[i];
+    }
+  }
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// ---------------------------------------------------------------- forward
+template <int V>
+__global__ void __launch_bounds__(kBlock) bn_stats(Geo g, const float* __restrict__ x, double2* __restrict__ part) {
+  const int c = blockIdx.y, p = blockIdx.x;
+  const float k = __ldg(x + (long long)c * g.HW);  // shift: first element of the channel
+  float s1 = 0.f, s2 = 0.f;
+  for_units<V>(g, c, p, [&](long long off) {
+    if (V == 4) {
+      const float4 v = ld4(x + off);
+      const float a = v.x - k, b = v.y - k, d = v.z - k, e = v.w - k;
+      s1 += (a + b) + (d + e);
+      s2 = fmaf(a, a, fmaf(b, b, fmaf(d, d, fmaf(e, e, s2))));
+    } else {
+      const float a = __ldg(x + off) - k;
+      s1 += a;
+      s2 = fmaf(a, a, s2);
+    }
+  });
+  double a = s1, b = s2;
+  block_sum2(a, b);
+  if (threadIdx.x == 0) part[c * g.P + p] = make_double2(a, b);
+}
+
+struct FwdArgs {
+  const float* x;
+  const float* r;  // residual (nullable)
+  float* y;
+  const float* gamma;
+  const float* beta;
+  float* running_mean;  // nullable
+  float* running_var;   // nullable
+  float* save_mean;
+  float* save_invstd;
+  const double2* part;
+  float momentum, eps;
+  int relu;
+};
+
+template <int V>
+__global__ void __launch_bounds__(kBlock) bn_apply(Geo g, FwdArgs a) {
+  const int c = blockIdx.y, p = blockIdx.x;
+  __shared__ float sh[2];
+  if (threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < g.P; ++i) {
+      const double2 q = a.part[c * g.P + i];
+      s1 += q.x;
+      s2 += q.y;
+    }
+    const double m = (double)g.N * g.HW;
+    const double k = (double)__ldg(a.x + (long long)c * g.HW);
+    const double d = s1 / m;
+    double var = s2 / m - d * d;
+    var = var > 0.0 ? var : 0.0;
+    const double mean = k + d;
+    const double invstd = 1.0 / sqrt(var + (double)a.eps);
+    sh[0] = (float)mean;
+    sh[1] = (float)invstd;
+    if (p == 0) {
+      a.save_mean[c] = (float)mean;
+      a.save_invstd[c] = (float)invstd;
+      if (a.running_mean) {
+        const double mo = a.momentum;
+        a.running_mean[c] = (float)((1.0 - mo) * a.running_mean[c] + mo * mean);
+        a.running_var[c] = (float)((1.0 - mo) * a.running_var[c] + mo * var * m / (m > 1.0 ? m - 1.0 : 1.0));
+      }
+    }
+  }
+  __syncthreads();
+  const float mean = sh[0];
+  const float sc = sh[1] * __ldg(a.gamma + c);
+  const float bt = __ldg(a.beta + c);
+  const bool relu = a.relu != 0;
+  const float* __restrict__ r = a.r;
+  for_units<V>(g, c, p, [&](long long off) {
+    if (V == 4) {
+      const float4 v = ld4(a.x + off);
+      float4 o = make_float4(fmaf(v.x - mean, sc, bt), fmaf(v.y - mean, sc, bt), fmaf(v.z - mean, sc, bt), fmaf(v.w - mean, sc, bt));
+      if (r) {
+        const float4 q = ld4(r + off);
+        o.x += q.x;
+        o.y += q.y;
+        o.z += q.z;
+        o.w += q.w;
+      }
+      if (relu) {
+        o.x = fmaxf(o.x, 0.f);
+        o.y = fmaxf(o.y, 0.f);
+        o.z = fmaxf(o.z, 0.f);
+        o.w = fmaxf(o.w, 0.f);
+      }
+      st4(a.y + off, o);
+    } else {
+      float o = fmaf(__ldg(a.x + off) - mean, sc, bt);
+      if (r) o += __ldg(r + off);
+      if (relu) o = fmaxf(o, 0.f);
+      a.y[off] = o;
+    }
+  });
+}
+
+// --------------------------------------------------------------- backward
+struct BwdArgs {
+  const float* x;
+  const float* y;  // forward output (ReLU mask); nullable when !relu
+  const float* dy;
+  const float* gamma;
+  const float* save_mean;
+  const float* save_invstd;
+  float* dx;
+  float* dr;  // residual grad (nullable)
+  float* dgamma;
+  float* dbeta;
+  double2* part;
+  int relu;
+};
+
+template <int V>
+__global__ void __launch_bounds__(kBlock) bn_bwd_reduce(Geo g, BwdArgs a) {
+  const int c = blockIdx.y, p = blockIdx.x;
+  const float mean = __ldg(a.save_mean + c), inv = __ldg(a.save_invstd + c);
+  const bool relu = a.relu != 0;
+  float sg = 0.f, sgx = 0.f;
+  for_units<V>(g, c, p, [&](long long off) {
+    if (V == 4) {
+      float4 d = ld4(a.dy + off);
+      if (relu) {
+        const float4 m = ld4(a.y + off);
+        d.x = m.x > 0.f ? d.x : 0.f;
+        d.y = m.y > 0.f ? d.y : 0.f;
+        d.z = m.z > 0.f ? d.z : 0.f;
+        d.w = m.w > 0.f ? d.w : 0.f;
+      }
+      const float4 v = ld4(a.x + off);
+      sg += (d.x + d.y) + (d.z + d.w);
+      sgx = fmaf(d.x, (v.x - mean) * inv, fmaf(d.y, (v.y - mean) * inv, fmaf(d.z, (v.z - mean) * inv, fmaf(d.w, (v.w - mean) * inv, sgx))));
+    } else {
+      float d = __ldg(a.dy + off);
+      if (relu && !(__ldg(a.y + off) > 0.f)) d = 0.f;
+      sg += d;
+      sgx = fmaf(d, (__ldg(a.x + off) - mean) * inv, sgx);
+    }
+  });
+  double s = sg, t = sgx;
+  block_sum2(s, t);
+  if (threadIdx.x == 0) a.part[c * g.P + p] = make_double2(s, t);
+}
+
+template <int V>
+__global__ void __launch_bounds__(kBlock) bn_bwd_apply(Geo g, BwdArgs a) {
+  const int c = blockIdx.y, p = blockIdx.x;
+  __shared__ float sh[2];
+  if (threadIdx.x == 0) {
+    double s = 0.0, t = 0.0;
+    for (int i = 0; i < g.P; ++i) {
+      const double2 q = a.part[c * g.P + i];
+      s += q.x;
+      t += q.y;
+    }
+    const double m = (double)g.N * g.HW;
+    sh[0] = (float)(s / m);
+    sh[1] = (float)(t / m);
+    if (p == 0) {
+      a.dbeta[c] = (float)s;
+      a.dgamma[c] = (float)t;
+    }
+  }
+  __syncthreads();
+  const float mg = sh[0], mgx = sh[1];
+  const float mean = __ldg(a.save_mean + c), inv = __ldg(a.save_invstd + c);
+  const float k = inv * __ldg(a.gamma + c);
+  const bool relu = a.relu != 0;
+  float* __restrict__ dr = a.dr;
+  for_units<V>(g, c, p, [&](long long off) {
+    if (V == 4) {
+      float4 d = ld4(a.dy + off);
+      if (relu) {
+        const float4 m = ld4(a.y + off);
+        d.x = m.x > 0.f ? d.x : 0.f;
+        d.y = m.y > 0.f ? d.y : 0.f;
+        d.z = m.z > 0.f ? d.z : 0.f;
+        d.w = m.w > 0.f ? d.w : 0.f;
+      }
+      const float4 v = ld4(a.x + off);
+      float4 o;
+      o.x = k * (d.x - mg - (v.x - mean) * inv * mgx);
+      o.y = k * (d.y - mg - (v.y - mean) * inv * mgx);
+      o.z = k * (d.z - mg - (v.z - mean) * inv * mgx);
+      o.w = k * (d.w - mg - (v.w - mean) * inv * mgx);
+      st4(a.dx + off, o);
+      if (dr) st4(dr + off, d);
+    } else {
+      float d = __ldg(a.dy + off);
+      if (relu && !(__ldg(a.y + off) > 0.f)) d = 0.f;
+      a.dx[off] = k * (d - mg - (__ldg(a.x + off) - mean) * inv * mgx);
+      if (dr) dr[off] = d;
+    }
+  });
+}
+
+thread_local char g_err[256];
+
+int fail(const char* what, cudaError_t e) {
+  snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+  return CANVAS_POST_ERR_CUDA;
+}
+
+int slices(int N, int C) {
+  // ~8 CTAs per SM (148 SMs), whole images per slice
+  int p = (148 * 8 + C - 1) / C;
+  if (p > N) p = N;
+  if (p < 1) p = 1;
+  return p;
+}
+
+bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int canvas_post_abi_version(void) { return CANVAS_POST_ABI_VERSION; }
+
+const char* canvas_post_last_error(void) { return g_err; }
+
+size_t canvas_bn_workspace(int64_t N, int64_t C, int64_t HW) {
+  (void)HW;
+  return (size_t)slices((int)N, (int)C) * (size_t)C * sizeof(double2);
+}
+
+int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const float* residual, float* y,
+                      const float* gamma, const float* beta, float* running_mean, float* running_var,
+                      float* save_mean, float* save_invstd, float momentum, float eps, int relu, void* workspace,
+                      void* stream) {
+  if (N < 1 || C < 1 || HW < 1 || !x || !y || !gamma || !beta || !save_mean || !save_invstd || !workspace ||
+      (running_mean == nullptr) != (running_var == nullptr) || N * C * HW >= (1LL << 40)) {
+    snprintf(g_err, sizeof g_err, "canvas_bn_forward: bad arguments");
+    return CANVAS_POST_ERR_ARGS;
+  }
+  Geo g = make_geo((int)N, (int)C, (int)HW, slices((int)N, (int)C));
+  if (!aligned16(x) || !aligned16(residual) || !aligned16(y)) g.V = 1, g.U = g.HW;
+  cudaStream_t s = (cudaStream_t)stream;
+  FwdArgs a{x, residual, y, gamma, beta, running_mean, running_var, save_mean, save_invstd, (const double2*)workspace, momentum, eps, relu};
+  const dim3 grid(g.P, g.C);
+  if (g.V == 4) {
+    bn_stats<4><<<grid, kBlock, 0, s>>>(g, x, (double2*)workspace);
+    bn_apply<4><<<grid, kBlock, 0, s>>>(g, a);
+  } else {
+    bn_stats<1><<<grid, kBlock, 0, s>>>(g, x, (double2*)workspace);
+    bn_apply<1><<<grid, kBlock, 0, s>>>(g, a);
+  }
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_bn_forward launch", e);
+}
+
+int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const float* dy,
+                       const float* gamma, const float* save_mean, const float* save_invstd, float* dx,
+                       float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace, void* stream) {
+  if (N < 1 || C < 1 || HW < 1 || !x || !dy || !gamma || !save_mean || !save_invstd || !dx || !dgamma || !dbeta ||
+      !workspace || (relu && !y) || N * C * HW >= (1LL << 40)) {
+    snprintf(g_err, sizeof g_err, "canvas_bn_backward: bad arguments");
+    return CANVAS_POST_ERR_ARGS;
+  }
+  Geo g = make_geo((int)N, (int)C, (int)HW, slices((int)N, (int)C));
+  if (!aligned16(x) || !aligned16(y) || !aligned16(dy) || !aligned16(dx) || !aligned16(dresidual)) g.V = 1, g.U = g.HW;
+  cudaStream_t s = (cudaStream_t)stream;
+  BwdArgs a{x, y, dy, gamma, save_mean, save_invstd, dx, dresidual, dgamma, dbeta, (double2*)workspace, relu};
+  const dim3 grid(g.P, g.C);
+  if (g.V == 4) {
+    bn_bwd_reduce<4><<<grid, kBlock, 0, s>>>(g, a);
+    bn_bwd_apply<4><<<grid, kBlock, 0, s>>>(g, a);
+  } else {
+    bn_bwd_reduce<1><<<grid, kBlock, 0, s>>>(g, a);
+    bn_bwd_apply<1><<<grid, kBlock, 0, s>>>(g, a);
+  }
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_bn_backward launch", e);
+}
+
+}  // extern "C"
