@@ -42,6 +42,22 @@ import torch.nn.functional as F  # noqa: E402
 from paper_2304_07741_b200 import zoo  # noqa: E402
 
 METRIC = "images/sec fwd+bwd (Canvas-ResNet-18, 224²) at 1/2/4/8 B200; % roofline/kernel"
+WORKLOADS = {
+    "resnet18": "config 2: torchvision ResNet-18, all 16 3x3 convs -> one Canvas kernel, fwd+bwd+SGD",
+    "resnet29": "config 3: CIFAR ResNet-29 (bottleneck, 30 standard convs) -> one Canvas kernel, fwd+bwd+SGD",
+    "resnext29_2x64d": "config 3: CIFAR ResNeXt-29 2x64d (21 standard convs; grouped 3x3 kept) -> one Canvas kernel, fwd+bwd+SGD",
+    "mobilenet_v2": "config 5: torchvision MobileNetV2, 32 standard convs -> one Canvas kernel, fwd+bwd+SGD",
+    "efficientnet_b0": "config 5: torchvision EfficientNet-B0, 60 standard convs -> one Canvas kernel, fwd+bwd+SGD",
+    "vgg16": "config 5: torchvision VGG-16, 12 standard 3x3 convs -> one Canvas kernel, fwd+bwd+SGD",
+}
+
+
+def metric_of(model: str) -> str:
+    if model == "resnet18":
+        return METRIC
+    from paper_2304_07741_b200.backbones import SPECS
+
+    return f"images/sec fwd+bwd (Canvas-{model}, {SPECS[model]['input'][-1]}²) on B200; % roofline/kernel"
 
 
 def peaks() -> dict:
@@ -52,28 +68,26 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
 
 
-def build_model(kernel: str, device=None, cpu_reference: bool = False, fuse_bn: bool = True):
-    import torchvision
+def build_model(kernel: str, device=None, cpu_reference: bool = False, fuse_bn: bool = True, model: str = "resnet18"):
+    """The workload network (backbones.py) with every standard conv replaced by
+    ``kernel``; the CPU reference path uses the oracle modules instead."""
+    import math
 
-    from paper_2304_07741_b200.module import replace
+    from paper_2304_07741_b200 import backbones
 
-    torch.manual_seed(0)
-    m = torchvision.models.resnet18(num_classes=1000)
     text = zoo.ALL[kernel]
+    factory = None
     if cpu_reference:
         from oracle.torch_ref import CanvasConvRef
 
         def factory(conv):
-            return CanvasConvRef(text, conv.in_channels, conv.out_channels, 8, 8, 3, 3, stride=conv.stride[0], g=4, seed=None)
+            k = conv.kernel_size[0]
+            g = math.gcd(min(conv.in_channels, conv.out_channels), 4)
+            return CanvasConvRef(text, conv.in_channels, conv.out_channels, 8, 8, k, k, stride=conv.stride[0], g=g, seed=None)
 
-        names = replace(m, text, factory=factory)
-    else:
-        names = replace(m, text, g=4)
-        if fuse_bn:
-            from paper_2304_07741_b200.post import fuse_backbone
-
-            assert fuse_backbone(m) == 20  # BN post-pass (+ReLU, +residual) on libcanvas_post
-    assert len(names) == 16, names
+    m, names = backbones.build(model, text, g=4, fuse_bn=fuse_bn, factory=factory)
+    if model == "resnet18":
+        assert len(names) == 16, names
     return m.to(device) if device is not None else m
 
 
@@ -107,14 +121,17 @@ class Clocks:
 class CpuReference:
     """CPU restatement (oracle/torch_ref.py, torch fp32, all host threads) of Canvas-ResNet-18."""
 
-    def __init__(self, kernel: str, batch: int = 2):
+    def __init__(self, kernel: str, batch: int = 2, model: str = "resnet18"):
+        from paper_2304_07741_b200.backbones import SPECS
+
         torch.set_num_threads(os.cpu_count() or 1)
-        self.kernel, self.batch = kernel, batch
-        self.m = build_model(kernel, cpu_reference=True)
+        self.kernel, self.batch, self.model = kernel, batch, model
+        self.m = build_model(kernel, cpu_reference=True, model=model)
         self.opt = torch.optim.SGD(self.m.parameters(), lr=0.01, momentum=0.9)
         g = torch.Generator().manual_seed(0)
-        self.x = torch.randn(batch, 3, 224, 224, generator=g)
-        self.y = torch.randint(0, 1000, (batch,), generator=g)
+        spec = SPECS[model]
+        self.x = torch.randn(batch, *spec["input"], generator=g)
+        self.y = torch.randint(0, spec["classes"], (batch,), generator=g)
 
     def step(self) -> None:
         self.opt.zero_grad(set_to_none=True)
@@ -129,7 +146,7 @@ class CpuReference:
             if time.perf_counter() - t0 >= budget_s:
                 break
         dt = time.perf_counter() - t0
-        return {"value": n * self.batch / dt, "unit": "images/s", "cores": torch.get_num_threads(), "steps": n, "seconds": round(dt, 2), "sample": f"{n} fwd+bwd+SGD steps of batch {self.batch} at 224^2 through Canvas-ResNet-18 ({self.kernel}) in torch fp32 on CPU ({self.cores_desc()})"}
+        return {"value": n * self.batch / dt, "unit": "images/s", "cores": torch.get_num_threads(), "steps": n, "seconds": round(dt, 2), "sample": f"{n} fwd+bwd+SGD steps of batch {self.batch} at {self.x.shape[-1]}^2 through Canvas-{self.model} ({self.kernel}) in torch fp32 on CPU ({self.cores_desc()})"}
 
     @staticmethod
     def cores_desc() -> str:
@@ -142,8 +159,8 @@ class CpuReference:
         return f"{os.cpu_count()} threads, {model}"
 
 
-def cpu_sample(kernel: str, budget_s: float, batch: int = 2) -> dict:
-    ref = CpuReference(kernel, batch)
+def cpu_sample(kernel: str, budget_s: float, batch: int = 2, model: str = "resnet18") -> dict:
+    ref = CpuReference(kernel, batch, model)
     ref.step()  # warm-up
     return ref.timed(budget_s)
 
@@ -152,7 +169,7 @@ def run_reference(args, rank: int, world: int) -> None:
     """Reference arm: the CPU restatement of the path on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    ref = CpuReference(args.kernel)
+    ref = CpuReference(args.kernel, model=args.model)
     for _ in range(args.warmup):
         ref.step()
     per_step = []
@@ -163,7 +180,7 @@ def run_reference(args, rank: int, world: int) -> None:
     val = statistics.mean(per_step)
     line = {
         "impl": "reference",
-        "metric": METRIC,
+        "metric": metric_of(args.model),
         "value": round(val, 3),
         "unit": "images/s",
         "n_gpus": world,
@@ -175,7 +192,7 @@ def run_reference(args, rank: int, world: int) -> None:
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"Canvas-ResNet-18 ({args.kernel}) fwd+bwd+SGD, 224^2, CPU restatement, batch {ref.batch} per timed sample", "kernel": args.kernel},
+        "config": {"workload": f"Canvas-{args.model} ({args.kernel}) fwd+bwd+SGD, {ref.x.shape[-1]}^2, CPU restatement, batch {ref.batch} per timed sample", "kernel": args.kernel, "model": args.model},
         "cpu_baseline": {"value": round(val, 3), "unit": "images/s", "cores": r["cores"], "kind": "port", "sample": r["sample"]},
         "e2e": {"value": round(val, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -189,6 +206,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--kernel", default="seed7_k1", choices=sorted(zoo.ALL))
+    ap.add_argument("--model", default="resnet18", help="workload backbone (backbones.SPECS): resnet18 = config 2 (default), resnet29 / resnext29_2x64d = config 3, mobilenet_v2 / efficientnet_b0 / vgg16 = config 5")
     ap.add_argument("--impl", default="canvas", choices=["canvas", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-seconds", type=float, default=30.0)
@@ -212,15 +230,18 @@ def main() -> None:
     torch.backends.cuda.matmul.allow_tf32 = False
     torch.backends.cudnn.benchmark = True
 
-    model = build_model(args.kernel, dev, fuse_bn=not args.no_fuse_bn)
+    from paper_2304_07741_b200.backbones import SPECS
+
+    spec = SPECS[args.model]
+    model = build_model(args.kernel, dev, fuse_bn=not args.no_fuse_bn, model=args.model)
     if world > 1:
         from torch.nn.parallel import DistributedDataParallel as DDP
 
         model = DDP(model, device_ids=[local], bucket_cap_mb=25, gradient_as_bucket_view=True)
     opt = torch.optim.SGD(model.parameters(), lr=0.01, momentum=0.9)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    x = torch.randn(args.batch, 3, 224, 224, device=dev, generator=gen)
-    lab = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+    x = torch.randn(args.batch, *spec["input"], device=dev, generator=gen)
+    lab = torch.randint(0, spec["classes"], (args.batch,), device=dev, generator=gen)
 
     def step(xb, yb):
         opt.zero_grad(set_to_none=True)
@@ -241,9 +262,19 @@ def main() -> None:
     from paper_2304_07741_b200.module import CanvasConv2d
 
     core = model.module if world > 1 else model
-    l1 = core.layer1[0].conv1
-    assert isinstance(l1, CanvasConv2d)
-    dp = l1.device_plan(x.new_empty(1, 64, 56, 56))
+    # dominant target: the first replaced conv at the network's finest resolution
+    # (ResNet-18: layer1.0.conv1, 64->64 at 56x56); its input shape is traced
+    shapes = {}
+    def _trace(mod, i, o):
+        shapes.setdefault(id(mod), tuple(i[0].shape))  # returns None: output unchanged
+
+    hooks = [m.register_forward_hook(_trace) for m in core.modules() if isinstance(m, CanvasConv2d)]
+    with torch.no_grad():
+        core(x[:1])
+    for h in hooks:
+        h.remove()
+    l1 = max((m for m in core.modules() if isinstance(m, CanvasConv2d)), key=lambda m: shapes[id(m)][2] * shapes[id(m)][3] * min(m.in_channels, m.out_channels) ** 2 / m.stride ** 2)
+    dp = l1.device_plan(x.new_empty(1, *shapes[id(l1)][1:]))
     recs = [i for i, L in enumerate(dp.plan.launches) if L.kind == "kernel" and L.flops_per_image and L.what.startswith("tc ")]
     per_rec_events = {}
     for i in recs:
@@ -324,6 +355,8 @@ def main() -> None:
         flops = float(L.flops_per_image) * args.batch
         ach = flops / (avg_ms * 1e-3) / 1e12
         kern.append({"kernel": L.name, "what": L.what, "launch_ms": round(avg_ms, 4), "launches_timed": len(ts), "useful_tflops": round(ach, 2), "frac_tf32": round(ach / tf32_peak, 4), "issued_frac_tf32": round(3 * ach / tf32_peak, 4), "total_ms": sum(ts)})
+    if not kern:
+        raise SystemExit(f"no tensor-core launch in the dominant target of {args.model}: nothing to put on the roofline")
     dom = max(kern, key=lambda r: r["total_ms"])
     L = dp.plan.launches[next(i for i in k_times if dp.plan.launches[i].name == dom["kernel"])]
     roofline = {
@@ -352,7 +385,7 @@ def main() -> None:
             pass
 
     line = {
-        "metric": METRIC,
+        "metric": metric_of(args.model),
         "value": round(value, 2),
         "unit": "images/s",
         "n_gpus": world,
@@ -365,11 +398,12 @@ def main() -> None:
         "dtype": "f32",
         "data": "synthetic",
         "config": {
-            "workload": "config 2: torchvision ResNet-18, all 16 3x3 convs -> one Canvas kernel, fwd+bwd+SGD",
+            "workload": WORKLOADS[args.model],
             "kernel": args.kernel,
+            "model": args.model,
             "global_batch": args.batch * world,
             "per_gpu_batch": args.batch,
-            "image": "3x224x224 synthetic N(0,1), random-init weights",
+            "image": "x".join(map(str, spec["input"])) + " synthetic N(0,1), random-init weights",
             "parallelism": f"dp{world}",
             "G": 4,
             "K": 3,
@@ -384,7 +418,7 @@ def main() -> None:
     if rank == 0 and world == 1 and not args.no_context:
         line["context"] = context_numbers(args, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = {k: v for k, v in cpu_sample(args.kernel, args.cpu_seconds).items() if k in ("value", "unit", "cores", "sample")}
+        line["cpu_baseline"] = {k: v for k, v in cpu_sample(args.kernel, args.cpu_seconds, model=args.model).items() if k in ("value", "unit", "cores", "sample")}
         line["cpu_baseline"]["kind"] = "port"
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -393,14 +427,15 @@ def main() -> None:
 
 
 def context_numbers(args, dev) -> dict:
-    """Unreplaced torchvision ResNet-18 (cuDNN, fp32 with TF32 off) for context only."""
-    import torchvision
+    """The unreplaced backbone (cuDNN, fp32 with TF32 off) for context only."""
+    from paper_2304_07741_b200.backbones import SPECS, backbone
 
     torch.manual_seed(0)
-    m = torchvision.models.resnet18(num_classes=1000).to(dev)
+    m = backbone(args.model).to(dev)
     opt = torch.optim.SGD(m.parameters(), lr=0.01, momentum=0.9)
-    x = torch.randn(args.batch, 3, 224, 224, device=dev)
-    y = torch.randint(0, 1000, (args.batch,), device=dev)
+    spec = SPECS[args.model]
+    x = torch.randn(args.batch, *spec["input"], device=dev)
+    y = torch.randint(0, spec["classes"], (args.batch,), device=dev)
 
     def step():
         opt.zero_grad(set_to_none=True)
@@ -416,7 +451,7 @@ def context_numbers(args, dev) -> dict:
         step()
     b.record()
     torch.cuda.synchronize()
-    return {"resnet18_cudnn_fp32_images_s": round(args.batch * 5 * 1000.0 / a.elapsed_time(b), 1)}
+    return {f"{args.model}_cudnn_fp32_images_s": round(args.batch * 5 * 1000.0 / a.elapsed_time(b), 1)}
 
 
 if __name__ == "__main__":

@@ -130,7 +130,10 @@ def replace(model: nn.Module, ir_text: str, *, g: int = 4, xs: dict | None = Non
                 if factory is not None:
                     new = factory(child)
                 else:
-                    new = CanvasConv2d(ir_text, child.in_channels, child.out_channels, child.kernel_size[0], child.stride[0], g=g, xs=txs, bias=child.bias is not None)
+                    # G must divide C = min(C_in, C_out) (group(G), App. A.1); targets whose C
+                    # it does not divide use the largest common divisor of the two
+                    tg = math.gcd(min(child.in_channels, child.out_channels), g)
+                    new = CanvasConv2d(ir_text, child.in_channels, child.out_channels, child.kernel_size[0], child.stride[0], g=tg, xs=txs, bias=child.bias is not None)
                 setattr(parent, cname, new)
                 done.append(f"{name}.{cname}" if name else cname)
     return done

@@ -171,7 +171,7 @@ def fuse_backbone(model: nn.Module) -> int:
             count += 1
 
     for m in list(model.modules()):
-        if isinstance(m, ResNet):
+        if isinstance(m, ResNet) or getattr(m, "_canvas_stem", False):
             swap(m, "bn1", True)
             m.relu = nn.Identity()
         elif isinstance(m, BasicBlock):
