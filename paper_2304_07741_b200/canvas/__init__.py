@@ -7,4 +7,4 @@ bit-identical symbolic results; the reference's own 45 tests run against this
 package (tests/test_reference_conformance.py).
 """
 
-from . import ir, micro_dag, primitives, shape_algebra, shape_solver  # noqa: F401
+from . import ir, micro_dag, primitives, sampler, shape_algebra, shape_solver  # noqa: F401

@@ -4,9 +4,10 @@
 
 One worker process per GPU (replicas only, no collective).  Each worker plans,
 compiles and times fwd+bwd of a kernel at config-1 shapes (N=8, C=64, 56^2,
-G=4, K=3).  The kernels are the IR texts emitted by
-Sampler(SamplerConfig(nodes=10, seed=7)).sample_many(256)
-(tests/golden/sampler_10_7_256.cir, sha256 f1638a90...).
+G=4, K=3).  The kernels are drawn by the sampler mirror,
+Sampler(SamplerConfig(nodes=10, seed=7)).sample_many(256) by default — the
+same texts the reference emits (tests/golden/sampler_10_7_256.cir, sha256
+f1638a90...; checked before the sweep when that config is used).
 Free variables are solved proportionally (x := smallest legal multiple >= C).
 """
 
@@ -28,11 +29,19 @@ def main():
     ap.add_argument("--count", type=int, default=256)
     ap.add_argument("--gpus", type=int, default=0)
     ap.add_argument("--out", default="")
+    ap.add_argument("--nodes", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=7)
     a = ap.parse_args()
     import torch
 
     n = a.gpus or torch.cuda.device_count()
-    texts = ["canvas-ir v1\n" + t for t in open(os.path.join(ROOT, "tests/golden/sampler_10_7_256.cir")).read().split("canvas-ir v1\n")[1:]][: a.count]
+    from paper_2304_07741_b200.canvas import ir
+    from paper_2304_07741_b200.canvas.sampler import Sampler, SamplerConfig
+
+    texts = [ir.emit(k) for k in Sampler(SamplerConfig(nodes=a.nodes, seed=a.seed)).sample_many(a.count)]
+    golden = os.path.join(ROOT, f"tests/golden/sampler_{a.nodes}_{a.seed}_{a.count}.cir")
+    if os.path.exists(golden):
+        assert "".join(texts) == open(golden).read(), "sampler mirror diverged from the reference golden"
     t0 = time.perf_counter()
     res = CandidateEvaluator(list(range(n))).run(texts)
     wall = time.perf_counter() - t0
