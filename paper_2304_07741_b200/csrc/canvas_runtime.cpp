@@ -62,6 +62,10 @@ struct Driver {
   CUresult (*cuGetErrorString)(CUresult, const char**);
   CUresult (*cuFuncSetAttribute)(CUfunction, int, int);
   CUresult (*cuEventRecord)(void*, CUstream);
+  // optional: inside CUDA-graph stream capture the profiling events must be
+  // recorded as external event nodes so they fire on every replay
+  CUresult (*cuEventRecordWithFlags)(void*, CUstream, unsigned) = nullptr;
+  CUresult (*cuStreamIsCapturing)(CUstream, int*) = nullptr;
 };
 
 // ----------------------------------------------------------------- NVRTC
@@ -112,6 +116,11 @@ Driver& driver() {
            sym(h, "cuLaunchKernel", d.cuLaunchKernel, w) && sym(h, "cuMemsetD8Async", d.cuMemsetD8Async, w) &&
            sym(h, "cuGetErrorString", d.cuGetErrorString, w) &&
            sym(h, "cuFuncSetAttribute", d.cuFuncSetAttribute, w) && sym(h, "cuEventRecord", d.cuEventRecord, w);
+    if (d.ok) {
+      std::string ignore;
+      sym(h, "cuEventRecordWithFlags", d.cuEventRecordWithFlags, ignore);
+      sym(h, "cuStreamIsCapturing", d.cuStreamIsCapturing, ignore);
+    }
     if (d.ok && d.cuInit(0) != 0) {
       d.ok = false;
       d.why = "cuInit failed (no usable GPU)";
@@ -202,6 +211,15 @@ struct canvas_plan {
 };
 
 namespace {
+
+constexpr unsigned kEventRecordExternal = 0x1;  // CU_EVENT_RECORD_EXTERNAL
+
+void record_event(Driver& d, void* ev, CUstream st, bool external) {
+  if (external)
+    d.cuEventRecordWithFlags(ev, st, kEventRecordExternal);
+  else
+    d.cuEventRecord(ev, st);
+}
 
 std::mutex g_mod_mu;
 std::unordered_map<std::string, CUmodule> g_modules;  // (device, source hash) -> module
@@ -334,6 +352,7 @@ int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, co
       for (int i = 0; i < 3; ++i) g[i] = (unsigned)r.grid[i].eval(batch);
       void* params[] = {&a};
       void* ev_end = nullptr;
+      bool ev_external = false;
       const int64_t ri = &r - p->recs.data();
       if (!p->prof.empty()) {
         std::lock_guard<std::mutex> lk(p->prof_mu);
@@ -341,14 +360,17 @@ int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, co
         if (it != p->prof.end() && !it->second.events.empty()) {
           auto& pr = it->second;
           const size_t slot = (size_t)(pr.count++ % (int64_t)(pr.events.size() / 2));
-          d.cuEventRecord(pr.events[2 * slot], st);
+          int capturing = 0;
+          if (d.cuStreamIsCapturing && d.cuEventRecordWithFlags) d.cuStreamIsCapturing(st, &capturing);
+          ev_external = capturing != 0;
+          record_event(d, pr.events[2 * slot], st, ev_external);
           ev_end = pr.events[2 * slot + 1];
         }
       }
       CUresult e = d.cuLaunchKernel(p->fns[r.kernel], g[0], g[1], g[2], (unsigned)r.block, 1, 1, (unsigned)r.smem, st, params,
                                     nullptr);
       if (e != 0) return fail(CANVAS_ERR_CUDA, "launch kernel " + std::to_string(r.kernel) + ": " + cu_err(e));
-      if (ev_end) d.cuEventRecord(ev_end, st);
+      if (ev_end) record_event(d, ev_end, st, ev_external);
     }
   }
   return CANVAS_OK;

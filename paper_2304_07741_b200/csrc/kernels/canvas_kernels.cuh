@@ -71,6 +71,24 @@ __device__ __forceinline__ void pointwise(const CanvasArgs& a) {
   }
 }
 
+// Plane-major variant: blockIdx.y = (image, channel plane) — block-uniform, so the
+// functor's channel index math (flat-channel decomposition, replica/tap
+// indices) runs once per warp on the uniform datapath — and the threads of
+// gridDim.x blocks walk the H*W pixels of that plane (coalesced).
+// gridDim.y is capped (~64 CTAs per SM over the launch), so each CTA strides
+// over planes: block turnover stays off the critical path and the per-CTA
+// setup is amortised.
+template <class F>
+__device__ __forceinline__ void pointwise_planes(const CanvasArgs& a) {
+  const long long planes = a.n * F::Q;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;  // x fastest: co-resident CTAs share planes
+  for (long long pq = blockIdx.y; pq < planes; pq += gridDim.y) {
+    const long long n = pq / F::Q;
+    const int q = (int)(pq - n * F::Q);
+    if (s < F::S) F::run(a, n, q, s);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2: softmax / row-dot over a channel span with SL threads per row.  When
 // rows are few and long (ResNet stage 4: 49 pixels x 512 channels) a thread

@@ -51,6 +51,8 @@ BETA_NONE, BETA_AFTER_FIRST, BETA_ALWAYS = 0, 1, 2
 POINTWISE_BLOCK = 256
 POINTWISE_VEC = int(os.environ.get("CANVAS_PW_VEC", "1"))  # elements per thread along the innermost dim
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
+PLANES_MIN_S = int(os.environ.get("CANVAS_PLANES_MIN_S", "128"))  # plane-major launch when H*W >= this (0 = off)
+PLANES_CTAS = int(os.environ.get("CANVAS_PLANES_CTAS", str(148 * 64)))  # CTAs of a plane-major launch (planes strided)
 GEMM_TILE = 64
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
@@ -269,6 +271,10 @@ class Fn:
         # computed node at raw (possibly out-of-range) coordinates whose value is
         # selected away when the predicates fail (no clamps, no OOB access)
         self.guard: tuple = ()
+        # plane-major functors: (channel extents, spatial extents) of the output whose
+        # flat index r = q * S + s is split into a block-uniform plane q and a
+        # per-thread spatial s (pointwise_planes)
+        self.planes: tuple | None = None
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -375,7 +381,7 @@ class Fn:
                 alpha = acc[live[-1][1]] // inner[live[-1][0]] if acc[live[-1][1]] % inner[live[-1][0]] == 0 else None
                 if alpha is None or any(acc[v] != alpha * inner[i] for i, v in live):
                     continue
-                sub = flat if j == 0 else self.ivar(f"{flat} % {math.prod(ext[j:])}")
+                sub = flat if j == 0 else self.suffix(flat, math.prod(ext[j:]))
                 for _, v in live:
                     del acc[v]
                 acc[sub] = acc.get(sub, 0) + alpha
@@ -384,6 +390,12 @@ class Fn:
         if const:
             terms.append(f"({const})")
         return self.ivar(" + ".join(terms) if terms else "0")
+
+    def suffix(self, flat: str, m: int) -> str:
+        """``flat % m``; in a plane-major functor r % m = s % m whenever m | S."""
+        if flat == "r" and self.planes is not None and math.prod(self.planes[1]) % m == 0:
+            return "s" if m == math.prod(self.planes[1]) else self.ivar(f"s % {m}")
+        return self.ivar(f"{flat} % {m}")
 
     def addr(self, d: TDesc, coords) -> str:
         off = self.offset(d, coords)
@@ -802,26 +814,61 @@ class Lowerer:
         self.p.kernel_names.append(name)
         return len(self.p.kernel_names) - 1
 
-    def functor_pointwise(self, name: str, per_image: int, body_fn) -> tuple[str, list]:
-        """Functor for ``canvas::pointwise``: one output element (or row) per call."""
+    def functor_pointwise(self, name: str, per_image: int, body_fn, planes=None) -> tuple[str, list]:
+        """Functor for ``canvas::pointwise``: one output element (or row) per call;
+        with ``planes`` = (channel ext, spatial ext), for ``canvas::pointwise_planes``."""
         f = Fn(self)
         f.pre = []
         f.computing = None
+        f.planes = planes
         body_fn(f)
-        src = [f"struct {name}_F {{", f"  static constexpr long long PER = {per_image}LL;", "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int r) {"]
+        if planes is None:
+            src = [f"struct {name}_F {{", f"  static constexpr long long PER = {per_image}LL;", "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int r) {"]
+        else:
+            Q, S = math.prod(planes[0]), math.prod(planes[1])
+            src = [f"struct {name}_F {{", f"  static constexpr int Q = {Q}, S = {S};", "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int q, const int s) {", f"    const int r = q * {S} + s;"]
         src += ["    " + s for s in f.pre]
         src += f.lines
         src += ["  }", "};"]
         return "\n".join(src) + "\n", f.local_slots
 
-    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1):
-        """``inner``: extent of the innermost output dim (per-thread vector width must divide it)."""
-        functor, slots = self.functor_pointwise(name, per_image, body_fn)
-        v = POINTWISE_VEC
-        launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {v}>(a); }}\n'
+    @staticmethod
+    def plane_split(ext, sp_ext, per_image):
+        """(channel ext, spatial ext) when a plane-major launch applies, else None."""
+        if not PLANES_MIN_S or ext is None:
+            return None
+        ext, nsp = tuple(ext), len(sp_ext)
+        S = math.prod(ext[len(ext) - nsp:]) if nsp else 1
+        if nsp == 0 or S < PLANES_MIN_S or math.prod(ext) != per_image:
+            return None
+        return ext[: len(ext) - nsp], ext[len(ext) - nsp:]
+
+    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1, node=None):
+        """``inner``: extent of the innermost output dim (per-thread vector width must divide it).
+        ``node``: the output node whose elements the threads map to; with H*W >= PLANES_MIN_S
+        the launch is plane-major (block-uniform channel plane, threads along pixels)."""
+        planes = self.plane_split(node.ext, node.sp_ext, per_image) if node is not None else None
+        functor, slots = self.functor_pointwise(name, per_image, body_fn, planes)
+        if planes is not None and "? __ldg(" in functor:
+            # guarded (Shift / Unfold) gathers: with block-uniform channel math the
+            # compiler turns the guards into branches around each load and the
+            # gathers serialise (measured 0.63 -> 0.75 ms on seed-7 #1 layer1 grad n7),
+            # so these keep the flat grid-stride mapping with predicated loads
+            planes = None
+            functor, slots = self.functor_pointwise(name, per_image, body_fn, None)
+        if planes is None:
+            v = POINTWISE_VEC
+            launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {v}>(a); }}\n'
+            block = POINTWISE_BLOCK
+            grid = (GridRule(per_image, 0, POINTWISE_BLOCK * v, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        else:
+            Q, S = math.prod(planes[0]), math.prod(planes[1])
+            chunks = -(-S // POINTWISE_BLOCK)
+            block = -(-(-(-S // chunks)) // 32) * 32
+            launcher = f'extern "C" __global__ void __launch_bounds__({block}) {name}(const CanvasArgs a) {{ canvas::pointwise_planes<{name}_F>(a); }}\n'
+            grid = (GridRule(0, chunks, 1), GridRule(Q, 0, 1, min(65535, max(1, PLANES_CTAS // chunks))), GridRule(0, 1, 1))
         k = self.add_kernel(name, functor, launcher)
-        grid = (GridRule(per_image, 0, POINTWISE_BLOCK * v, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
-        self.p.launches.append(Launch("kernel", phase, name, k, POINTWISE_BLOCK, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
 
     # ---- forward
     def fwd_targets(self, v: int) -> list:
@@ -855,7 +902,7 @@ class Lowerer:
             tg = self.fwd_targets(v)
             io = 4 * (nd.numel + self._input_numel(nd))
             if nd.op == "fold":
-                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_fold(f, v, tg), 0, beta, f"fold {nd.attr['mode']} -> n{v}", io, 0, inner=nd.ext[-1] if nd.ext else 1)
+                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_fold(f, v, tg), 0, beta, f"fold {nd.attr['mode']} -> n{v}", io, 0, inner=nd.ext[-1] if nd.ext else 1, node=nd)
             elif nd.op == "softmax":
                 pre, span, post = self.softmax_geom(nd)
                 rows = math.prod(pre) * math.prod(post)
@@ -868,7 +915,7 @@ class Lowerer:
             elif nd.op == "fc":
                 self.lower_fc_fwd(name, v, tg, beta)
             else:
-                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_map(f, v, tg), 0, beta, f"pointwise -> n{v}", io, 0, inner=nd.ext[-1] if nd.ext else 1)
+                self.launch_pointwise(name, nd.numel, lambda f, v=v, tg=tg: self.body_map(f, v, tg), 0, beta, f"pointwise -> n{v}", io, 0, inner=nd.ext[-1] if nd.ext else 1, node=nd)
 
     def _input_numel(self, nd) -> int:
         """Compulsory reads: materialised tensors the node's expression touches (once each)."""
@@ -885,6 +932,13 @@ class Lowerer:
         return tot
 
     def coords_of(self, f: Fn, nd) -> tuple:
+        if f.planes is not None and tuple(nd.ext) == f.planes[0] + f.planes[1]:
+            qc = f.decompose("q", f.planes[0]) if f.planes[0] else []
+            sc = f.decompose("s", f.planes[1])
+            c = tuple(qc) + tuple(sc)
+            if len(c) > 1:
+                f.flat_of.setdefault(c, ("r", tuple(nd.ext)))
+            return c
         return tuple(f.decompose("r", nd.ext))
 
     def body_map(self, f: Fn, v: int, targets) -> None:
@@ -1026,7 +1080,7 @@ class Lowerer:
                 for d, b in targets:
                     f.store(d, c, acc, b)
 
-            self.launch_pointwise(name, nu.numel, body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1)
+            self.launch_pointwise(name, nu.numel, body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1, node=nu)
             return
         # A(m,k) = W[m*K + k];  B(n,k,s) = val(v)(decompose k | decompose s)
         fa = Fn(self)
@@ -1232,7 +1286,7 @@ class Lowerer:
                 beta = dx_beta if u == 0 else BETA_NONE
                 d = self.grad_desc[u]
                 name = f"k{len(p.kernel_names)}_bwd_grad{u}"
-                self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0, inner=nu.ext[-1] if nu.ext else 1)
+                self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0, inner=nu.ext[-1] if nu.ext else 1, node=nu)
             # 2) adjoint kernels of the producer edge that need dL/du as a whole
             if nu.op == "fc":
                 self.lower_fc_bwd(u, dx_beta)
@@ -1321,7 +1375,7 @@ class Lowerer:
                 f.close()
                 f.store(dd, c, acc, beta != BETA_NONE)
 
-            self.launch_pointwise(name, nv.numel, body, 1, beta, f"dgrad_small {O}x{K} n{u}->n{v}", 4 * (nu.numel + nv.numel), flops, inner=nv.ext[-1] if nv.ext else 1)
+            self.launch_pointwise(name, nv.numel, body, 1, beta, f"dgrad_small {O}x{K} n{u}->n{v}", 4 * (nu.numel + nv.numel), flops, inner=nv.ext[-1] if nv.ext else 1, node=nv)
         else:
             fa = Fn(self)
             fa.pre = []

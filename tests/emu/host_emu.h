@@ -38,6 +38,13 @@ void pointwise(const CanvasArgs& a) {
 }
 
 template <class F>
+void pointwise_planes(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int q = 0; q < F::Q; ++q)
+      for (int s = 0; s < F::S; ++s) F::run(a, n, q, s);
+}
+
+template <class F>
 void gemm_nk(const CanvasArgs& a) {
   const long long T = a.n * (long long)F::S;
   float* col = new float[F::K];

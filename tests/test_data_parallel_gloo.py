@@ -3,8 +3,9 @@
 Canvas kernels are per-image independent and FC wgrad is a sum over images
 (SURVEY §8e-1), so averaging per-rank gradients of equal shards equals the
 full-batch gradient.  Checked with the CPU reference module and
-torch.distributed's allreduce — the same collective bench.py's DDP issues
-over NCCL on GPUs.
+torch.distributed's allreduce — the per-gradient all-reduce (sum, then / world)
+bench.py captures into its CUDA-graph step over NCCL on GPUs (DDP without
+graphs issues the same sums, bucketed).
 """
 
 import os

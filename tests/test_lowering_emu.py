@@ -65,3 +65,28 @@ def test_blob_roundtrip_fields():
     assert b[:8] == b"CNVSBLOB"
     assert p.copies == 2 and p.mode == "concat" and p.y_copy_off == 64 * 28 * 28
     assert np.frombuffer(b[8:16], np.int64)[0] == 1
+
+
+@pytest.fixture
+def planes_everywhere(monkeypatch):
+    """Lower with plane-major pointwise launches down to 1-pixel planes."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "PLANES_MIN_S", 1)
+    executor._plan_cached.cache_clear()
+    yield
+    executor._plan_cached.cache_clear()
+
+
+@pytest.mark.parametrize("name", list(zoo.ALL))
+def test_plane_major_pointwise(name, planes_everywhere):
+    case = reference(zoo.ALL[name], 16, 32, 10, 9, stride=2)
+    assert any("pointwise_planes" in k for k in case.plan.source.splitlines())
+    assert_close(case, *emu_run(case), f"{name} plane-major")
+
+
+def test_plane_major_sweep_first40(planes_everywhere):
+    texts = ["canvas-ir v1\n" + t for t in open("tests/golden/sampler_10_7_256.cir").read().split("canvas-ir v1\n")[1:]]
+    for i in range(40):
+        case = reference(texts[i], 16, 16, 8, 7)
+        assert_close(case, *emu_run(case), f"sweep #{i} plane-major")
