@@ -657,7 +657,12 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
 #pragma unroll
           for (int mb = 0; mb < 4; ++mb) {
             const float v = F::B(a, (long long)pn[mb], kc, ps[mb]);
-            va[q][mb] = (((okmask >> mb) & 1u) && k < F::K) ? v : 0.f;
+            const bool ok = ((okmask >> mb) & 1u) && k < F::K;
+            va[q][mb] = ok ? v : 0.f;
+            // operand write-back for the wgrad (coalesced along the lane = pixel)
+            if constexpr (F::SAVE_B) {
+              if (ok) F::save_b(a, (long long)pn[mb], k, ps[mb], v);
+            }
           }
         }
       };

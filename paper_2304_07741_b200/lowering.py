@@ -51,6 +51,7 @@ BETA_NONE, BETA_AFTER_FIRST, BETA_ALWAYS = 0, 1, 2
 POINTWISE_BLOCK = 256
 POINTWISE_VEC = int(os.environ.get("CANVAS_PW_VEC", "1"))  # elements per thread along the innermost dim
 POINTWISE_CAP = 148 * 8 * 4  # grid-stride: 4 waves of 8 x 256-thread CTAs per SM
+SAVE_OPERAND = os.environ.get("CANVAS_SAVE_OPERAND", "0") == "1"  # FC forward keeps a computed operand for the wgrad (measured slower: off)
 PLANES_MIN_S = int(os.environ.get("CANVAS_PLANES_MIN_S", "128"))  # plane-major launch when H*W >= this (0 = off)
 PLANES_CTAS = int(os.environ.get("CANVAS_PLANES_CTAS", str(148 * 64)))  # CTAs of a plane-major launch (planes strided)
 GEMM_TILE = 64
@@ -1098,10 +1099,31 @@ class Lowerer:
             for d, b in targets:
                 f.store(d, c, val, b)
 
-        self.emit_gemm_nk(name, fa, a_expr, bfn, sfn, M=O, K=K, S=S, phase=0, beta=beta, what=f"fc {O}x{K}x{S} -> n{u}", nbytes=io, flops=flops)
+        # a computed operand (not a pure view of a materialised tensor) whose FC
+        # has a tensor-core wgrad: the forward producers also write the operand
+        # they evaluate, so the wgrad's B is a plain coalesced load instead of
+        # re-evaluating the producer chain (computed-operand GEMMs are
+        # bound by operand evaluation, not by the tensor pipe)
+        save = None
+        if SAVE_OPERAND and v not in self.fwd_desc and nv.op not in VIEW_OPS and O > 16 and K >= 32:
+            sdesc = self._new_saved(nv.ext)
+            sidx = len(self.p.saved) - 1
 
-    def emit_gemm_nk(self, name, fa: Fn, a_expr: str, bfn, sfn, M, K, S, phase, beta, what, nbytes, flops) -> None:
-        """C[n][m][s] = sum_k A(m,k) * B(n,k,s) through canvas::gemm_nk (one shared slot table)."""
+            def save(f, sdesc=sdesc):
+                c = tuple(f.decompose("k", nv.ch_ext)) + tuple(f.decompose("s", nv.sp_ext))
+                f.store(sdesc, c, "val", False)
+
+        saved = self.emit_gemm_nk(name, fa, a_expr, bfn, sfn, M=O, K=K, S=S, phase=0, beta=beta, what=f"fc {O}x{K}x{S} -> n{u}", nbytes=io, flops=flops, save=save)
+        if save is not None:
+            if saved:
+                self.fwd_desc[v] = sdesc  # later readers (the wgrad B operand) load it
+            else:
+                self.p.saved[sidx] = SizeRule(0, 1, 0)  # path without operand write-back: no buffer
+
+    def emit_gemm_nk(self, name, fa: Fn, a_expr: str, bfn, sfn, M, K, S, phase, beta, what, nbytes, flops, save=None) -> bool:
+        """C[n][m][s] = sum_k A(m,k) * B(n,k,s) through canvas::gemm_nk (one shared slot table).
+        ``save(f)``: emit the store of B's value ``val`` at (n, k, s) — the operand
+        write-back; honoured (returns True) only on the non-persistent tcgen05 path."""
         fb = Fn(self)
         fb.pre = []
         fb.computing = None
@@ -1122,9 +1144,26 @@ class Lowerer:
         ]
         lines += ["    " + s for s in fb.pre] + fb.lines + [f"    return {bval};", "  }"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
-        lines += ["    " + s for s in fs.pre] + fs.lines + ["  }", "};"]
+        lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
+        tc = self.use_tc and M >= 8 and K >= 16
+        nacc0 = 1
+        while nacc0 < 4 and K > TC_ACC_K * nacc0:
+            nacc0 *= 2
+        persistent = tc and TC_PERSIST and K < 4 * tc_tile(M, min(TC_NTMAX, 512 // nacc0))[0]
+        do_save = save is not None and tc and not persistent and TC_A_MN == "true"
+        if do_save:
+            fv = Fn(self)
+            fv.pre = []
+            fv.computing = None
+            fv.local_slots = fa.local_slots
+            save(fv)
+            lines += ["  static constexpr bool SAVE_B = true;", "  static __device__ __forceinline__ void save_b(const CanvasArgs& a, const long long n, const int k, const int s, const float val) {"]
+            lines += ["    " + s for s in fv.pre] + fv.lines + ["  }"]
+        else:
+            lines += ["  static constexpr bool SAVE_B = false;", "  static __device__ __forceinline__ void save_b(const CanvasArgs&, const long long, const int, const int, const float) {}"]
+        lines += ["};"]
         functor = "\n".join(lines) + "\n"
-        if self.use_tc and M >= 8 and K >= 16:
+        if tc:
             # long reductions run over NACC TMEM accumulators (<= TC_ACC_K terms each),
             # which caps the column tile so NACC x NT fits the 512 TMEM columns
             nacc = 1
@@ -1155,7 +1194,7 @@ class Lowerer:
                 self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
                 grid = (GridRule(S * nct, 0, 128, SMS), GridRule(0, 1, 1), GridRule(0, 1, 1))
                 self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=psmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
-                return
+                return False
             # 2 CTAs x 8 producer warps when a 2-stage ring pairs on an SM, else 1 CTA x 16 warps
             pw = TC_PIX_PW if TC_PIX_PW else (8 if smem <= TC_SMEM_PAIR else 16)
             threads = (pw + 2) * 32
@@ -1170,11 +1209,12 @@ class Lowerer:
             self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
             grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
             self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
-            return
+            return do_save
         launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_nk<{name}_F>(a); }}\n'
         k = self.add_kernel(name, functor, launcher)
         grid = (GridRule(S, 0, GEMM_TILE), GridRule(0, M, GEMM_TILE), GridRule(0, 1, 1))
         self.p.launches.append(Launch("kernel", phase, name, k, 256, grid, tuple(fa.local_slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+        return False
 
     def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops) -> None:
         """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
@@ -1412,7 +1452,7 @@ class Lowerer:
         fix = lambda s: p.slot_ws(-1 - s) if s < 0 else s  # noqa: E731
         for L in p.launches:
             L.slots = tuple(fix(s) for s in L.slots)
-        header = '#include "canvas_kernels.cuh"\n'
+        header = ("#define CANVAS_RAW_HI 1\n" if os.environ.get("CANVAS_RAW_HI") == "1" else "") + '#include "canvas_kernels.cuh"\n'
         p.source = header + "\n".join(self.kernels)
         del nsv
 

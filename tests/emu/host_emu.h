@@ -51,7 +51,10 @@ void gemm_nk(const CanvasArgs& a) {
   for (long long t = 0; t < T; ++t) {
     const long long n = t / F::S;
     const int s = (int)(t - n * F::S);
-    for (int k = 0; k < F::K; ++k) col[k] = F::B(a, n, k, s);
+    for (int k = 0; k < F::K; ++k) {
+      col[k] = F::B(a, n, k, s);
+      if constexpr (F::SAVE_B) F::save_b(a, n, k, s, col[k]);
+    }
     for (int m = 0; m < F::M; ++m) {
       float acc = 0.f;
       for (int k = 0; k < F::K; ++k) acc = std::fma(F::A(a, m, k), col[k], acc);

@@ -90,3 +90,17 @@ def test_plane_major_sweep_first40(planes_everywhere):
     for i in range(40):
         case = reference(texts[i], 16, 16, 8, 7)
         assert_close(case, *emu_run(case), f"sweep #{i} plane-major")
+
+
+@pytest.mark.parametrize("cin,cout,stride", [(32, 32, 1), (32, 64, 2), (64, 32, 1)])
+def test_operand_writeback(cin, cout, stride, monkeypatch):
+    """seed-7 #1's K=9C FC: the forward GEMM writes its computed operand and the
+    wgrad reads it back (SAVE_B), per Fig.-2 copy (optional path, off by default)."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "SAVE_OPERAND", True)
+    executor._plan_cached.cache_clear()
+    case = reference(zoo.SEED7_K1, cin, cout, 9, 8, stride=stride, n=2)
+    executor._plan_cached.cache_clear()
+    assert "SAVE_B = true" in case.plan.source
+    assert_close(case, *emu_run(case), f"write-back {cin}->{cout} s{stride}")
