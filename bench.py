@@ -305,7 +305,10 @@ def main() -> None:
                 per_step_launches += p.launches(0) + p.launches(1)
     from paper_2304_07741_b200.post import FusedBatchNorm2d
 
+    from paper_2304_07741_b200.post import FusedMaxPool2d
+
     per_step_launches += 4 * sum(isinstance(m, FusedBatchNorm2d) for m in core.modules())  # stats+apply, reduce+apply
+    per_step_launches += 2 * sum(isinstance(m, FusedMaxPool2d) for m in core.modules())  # fwd, bwd
 
     # --- CUDA graph of the whole step (forward, backward, all-reduce, SGD): one
     # replay per step, so host launch overhead leaves the critical path.  The

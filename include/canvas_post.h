@@ -1,7 +1,8 @@
 /*
  * canvas_post.h — C ABI of the post-pass of a replaced conv
  * (libcanvas_post.so): training-mode BatchNorm2d over the Canvas kernel's
- * output with the block's ReLU and residual add fused in.
+ * output with the block's ReLU and residual add fused in, and the stem
+ * max-pool of the ResNet backbones (deterministic gather backward).
  *
  * What it replaces in the reference:
  *   SPEC.md:658 (trainer_plugin.build_module, "BN post-pass" after the FC of
@@ -53,6 +54,16 @@ int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const fl
 int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const float* dy,
                        const float* gamma, const float* save_mean, const float* save_invstd, float* dx,
                        float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace, void* stream);
+
+/* Max-pool (square window K, stride S, padding P, no dilation, floor mode) of
+ * [N, C, H, W]: y [N, C, OH, OW] and the winner's window slot (kh*K + kw, one
+ * byte per output; first maximum in row-major order, NaN propagates). */
+int canvas_maxpool2d_forward(int64_t N, int64_t C, int64_t H, int64_t W, int K, int S, int P, const float* x, float* y,
+                             uint8_t* argmax, void* stream);
+
+/* dx [N, C, H, W] (written) from dy [N, C, OH, OW] and the forward's argmax. */
+int canvas_maxpool2d_backward(int64_t N, int64_t C, int64_t H, int64_t W, int K, int S, int P, const float* dy,
+                              const uint8_t* argmax, float* dx, void* stream);
 
 const char* canvas_post_last_error(void);
 

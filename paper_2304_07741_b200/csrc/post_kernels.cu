@@ -30,6 +30,8 @@
 #include <stdio.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "canvas_post.h"
 
 namespace {
@@ -301,6 +303,134 @@ __global__ void __launch_bounds__(kBlock) bn_bwd_apply(Geo g, BwdArgs a) {
   });
 }
 
+
+// ------------------------------------------------------------- max-pool
+// The stem max-pool of the ResNet backbones (3x3, stride 2, pad 1) between the
+// fused stem BN+ReLU and the first replaced conv.  Forward: one thread per
+// output, first maximum in row-major window order wins (NaN propagates, torch
+// semantics), the winner's window slot kept as one byte.  Backward is a
+// gather — each input element sums, in a fixed order, the gradients of the
+// (at most ceil(K/S)^2) windows whose recorded winner it is: no atomics.
+struct PoolGeo {
+  int N, C, H, W, K, S, P, OH, OW;
+};
+
+// Plane-major grid (blockIdx.y strides over N*C planes, 32-bit index math in a
+// plane); the common 3x3 / stride 2 / pad 1 stem is a compile-time instance
+// (KK = 0: runtime geometry).
+template <int KK, int SS, int PP>
+__global__ void __launch_bounds__(kBlock) maxpool_fwd(PoolGeo g, const float* __restrict__ x, float* __restrict__ y,
+                                                      uint8_t* __restrict__ idx) {
+  const int K = KK ? KK : g.K, S = KK ? SS : g.S, P = KK ? PP : g.P;
+  const int j = blockIdx.x * kBlock + threadIdx.x;
+  if (j >= g.OH * g.OW) return;
+  const int oh = j / g.OW, ow = j - oh * g.OW;
+  const long long planes = (long long)g.N * g.C;
+  for (long long pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const float* xp = x + pl * g.H * g.W;
+    float m = -INFINITY;
+    int best = 0;
+#pragma unroll
+    for (int kh = 0; kh < (KK ? KK : 15); ++kh) {
+      if (!KK && kh >= K) break;
+      const int h = oh * S - P + kh;
+      if ((unsigned)h >= (unsigned)g.H) continue;
+#pragma unroll
+      for (int kw = 0; kw < (KK ? KK : 15); ++kw) {
+        if (!KK && kw >= K) break;
+        const int w = ow * S - P + kw;
+        if ((unsigned)w >= (unsigned)g.W) continue;
+        const float v = __ldg(xp + h * g.W + w);
+        if (v > m || isnan(v)) {
+          m = v;
+          best = kh * K + kw;
+        }
+      }
+    }
+    const long long o = pl * g.OH * g.OW + j;
+    y[o] = m;
+    idx[o] = (uint8_t)best;
+  }
+}
+
+// 3x3 / stride 2 / pad 1 backward in closed form: an even input row is covered
+// by one window row (kh = 1), an odd one by two (kh = 2 then kh = 0), same for
+// columns, so each input sums at most four window gradients (increasing oh, ow).
+__global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2(PoolGeo g, const float* __restrict__ dy,
+                                                          const uint8_t* __restrict__ idx, float* __restrict__ dx) {
+  const int j = blockIdx.x * kBlock + threadIdx.x;
+  if (j >= g.H * g.W) return;
+  const int h = j / g.W, w = j - h * g.W;
+  int rows = 1, oh0, kh0, oh1 = 0, kh1 = 0;
+  if (h & 1) {
+    oh0 = h >> 1, kh0 = 2, oh1 = (h + 1) >> 1, kh1 = 0;
+    rows = oh1 < g.OH ? 2 : 1;
+  } else {
+    oh0 = h >> 1, kh0 = 1;
+  }
+  int cols = 1, ow0, kw0, ow1 = 0, kw1 = 0;
+  if (w & 1) {
+    ow0 = w >> 1, kw0 = 2, ow1 = (w + 1) >> 1, kw1 = 0;
+    cols = ow1 < g.OW ? 2 : 1;
+  } else {
+    ow0 = w >> 1, kw0 = 1;
+  }
+  const long long planes = (long long)g.N * g.C;
+  for (long long pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const float* dyp = dy + pl * g.OH * g.OW;
+    const uint8_t* ip = idx + pl * g.OH * g.OW;
+    float acc = 0.f;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (r >= rows) break;
+      const int oh = r ? oh1 : oh0, kh = r ? kh1 : kh0;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        if (c >= cols) break;
+        const int o = oh * g.OW + (c ? ow1 : ow0);
+        const int slot = kh * 3 + (c ? kw1 : kw0);
+        const float d = __ldg(dyp + o);
+        acc += __ldg(ip + o) == slot ? d : 0.f;
+      }
+    }
+    dx[pl * g.H * g.W + j] = acc;
+  }
+}
+
+template <int KK, int SS, int PP>
+__global__ void __launch_bounds__(kBlock) maxpool_bwd(PoolGeo g, const float* __restrict__ dy,
+                                                      const uint8_t* __restrict__ idx, float* __restrict__ dx) {
+  const int K = KK ? KK : g.K, S = KK ? SS : g.S, P = KK ? PP : g.P;
+  const int j = blockIdx.x * kBlock + threadIdx.x;
+  if (j >= g.H * g.W) return;
+  const int h = j / g.W, w = j - h * g.W;
+  const long long planes = (long long)g.N * g.C;
+  for (long long pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const float* dyp = dy + pl * g.OH * g.OW;
+    const uint8_t* ip = idx + pl * g.OH * g.OW;
+    float acc = 0.f;
+#pragma unroll
+    for (int kh = (KK ? KK : 15) - 1; kh >= 0; --kh) {  // windows in increasing oh
+      if (!KK && kh >= K) continue;
+      const int t = h + P - kh;
+      if (t < 0 || t % S) continue;
+      const int oh = t / S;
+      if (oh >= g.OH) continue;
+#pragma unroll
+      for (int kw = (KK ? KK : 15) - 1; kw >= 0; --kw) {
+        if (!KK && kw >= K) continue;
+        const int u = w + P - kw;
+        if (u < 0 || u % S) continue;
+        const int ow = u / S;
+        if (ow >= g.OW) continue;
+        const int o = oh * g.OW + ow;
+        if (__ldg(ip + o) == kh * K + kw) acc += __ldg(dyp + o);
+      }
+    }
+    dx[pl * g.H * g.W + j] = acc;
+  }
+}
+
 thread_local char g_err[256];
 
 int fail(const char* what, cudaError_t e) {
@@ -378,6 +508,40 @@ int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const f
   }
   const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_bn_backward launch", e);
+}
+
+int canvas_maxpool2d_forward(int64_t N, int64_t C, int64_t H, int64_t W, int K, int S, int P, const float* x, float* y,
+                             uint8_t* argmax, void* stream) {
+  if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || K > 15 || S < 1 || P < 0 || 2 * P > K || !x || !y || !argmax) {
+    snprintf(g_err, sizeof g_err, "canvas_maxpool2d_forward: bad arguments");
+    return CANVAS_POST_ERR_ARGS;
+  }
+  PoolGeo g{(int)N, (int)C, (int)H, (int)W, K, S, P, (int)((H + 2 * P - K) / S + 1), (int)((W + 2 * P - K) / S + 1)};
+  const int bx = (g.OH * g.OW + kBlock - 1) / kBlock;
+  const dim3 grid(bx, (unsigned)std::min<long long>(N * C, std::max(1, 148 * 32 / bx)));
+  if (K == 3 && S == 2 && P == 1)
+    maxpool_fwd<3, 2, 1><<<grid, kBlock, 0, (cudaStream_t)stream>>>(g, x, y, argmax);
+  else
+    maxpool_fwd<0, 0, 0><<<grid, kBlock, 0, (cudaStream_t)stream>>>(g, x, y, argmax);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_maxpool2d_forward launch", e);
+}
+
+int canvas_maxpool2d_backward(int64_t N, int64_t C, int64_t H, int64_t W, int K, int S, int P, const float* dy,
+                              const uint8_t* argmax, float* dx, void* stream) {
+  if (N < 1 || C < 1 || H < 1 || W < 1 || K < 1 || K > 15 || S < 1 || P < 0 || 2 * P > K || !dy || !argmax || !dx) {
+    snprintf(g_err, sizeof g_err, "canvas_maxpool2d_backward: bad arguments");
+    return CANVAS_POST_ERR_ARGS;
+  }
+  PoolGeo g{(int)N, (int)C, (int)H, (int)W, K, S, P, (int)((H + 2 * P - K) / S + 1), (int)((W + 2 * P - K) / S + 1)};
+  const int bx = (int)((H * W + kBlock - 1) / kBlock);
+  const dim3 grid(bx, (unsigned)std::min<long long>(N * C, std::max(1, 148 * 32 / bx)));
+  if (K == 3 && S == 2 && P == 1)
+    maxpool_bwd_k3s2<<<grid, kBlock, 0, (cudaStream_t)stream>>>(g, dy, argmax, dx);
+  else
+    maxpool_bwd<0, 0, 0><<<grid, kBlock, 0, (cudaStream_t)stream>>>(g, dy, argmax, dx);
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_maxpool2d_backward launch", e);
 }
 
 }  // extern "C"

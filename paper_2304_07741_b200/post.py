@@ -51,6 +51,8 @@ def load_library() -> ctypes.CDLL:
         p = c.c_void_p
         lib.canvas_bn_forward.argtypes = [c.c_int64] * 3 + [p] * 9 + [c.c_float, c.c_float, c.c_int, p, p]
         lib.canvas_bn_backward.argtypes = [c.c_int64] * 3 + [p] * 10 + [c.c_int, p, p]
+        lib.canvas_maxpool2d_forward.argtypes = [c.c_int64] * 4 + [c.c_int] * 3 + [p] * 4
+        lib.canvas_maxpool2d_backward.argtypes = [c.c_int64] * 4 + [c.c_int] * 3 + [p] * 4
         if lib.canvas_post_abi_version() != ABI_VERSION:
             raise PostError("libcanvas_post.so ABI version mismatch")
         _lib = lib
@@ -140,6 +142,53 @@ class FusedBatchNorm2d(nn.BatchNorm2d):
         return super().extra_repr() + f", relu={self.relu}"
 
 
+class _PoolFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, k, s, p):
+        lib = load_library()
+        x = x.contiguous()
+        n, c, h, w = x.shape
+        oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+        y = torch.empty((n, c, oh, ow), device=x.device, dtype=x.dtype)
+        idx = torch.empty((n, c, oh, ow), device=x.device, dtype=torch.uint8)
+        st = torch.cuda.current_stream(x.device).cuda_stream
+        _check(lib.canvas_maxpool2d_forward(n, c, h, w, k, s, p, x.data_ptr(), y.data_ptr(), idx.data_ptr(), st))
+        ctx.geo = (n, c, h, w, k, s, p)
+        ctx.save_for_backward(idx)
+        ctx.mark_non_differentiable(idx)
+        return y
+
+    @staticmethod
+    def backward(ctx, dy):
+        lib = load_library()
+        (idx,) = ctx.saved_tensors
+        n, c, h, w, k, s, p = ctx.geo
+        dy = dy.contiguous()
+        dx = torch.empty((n, c, h, w), device=dy.device, dtype=dy.dtype)
+        st = torch.cuda.current_stream(dy.device).cuda_stream
+        _check(lib.canvas_maxpool2d_backward(n, c, h, w, k, s, p, dy.data_ptr(), idx.data_ptr(), dx.data_ptr(), st))
+        return dx, None, None, None
+
+
+class FusedMaxPool2d(nn.MaxPool2d):
+    """``nn.MaxPool2d`` (square, no dilation, floor mode, fp32) on
+    libcanvas_post: byte argmax, deterministic gather backward."""
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if not x.is_cuda:
+            return super().forward(x)
+        if x.dtype != torch.float32 or x.dim() != 4:
+            raise TypeError("FusedMaxPool2d: fp32 NCHW input expected")
+        return _PoolFn.apply(x, self.kernel_size, self.stride, self.padding)
+
+    @classmethod
+    def from_pool(cls, m: nn.MaxPool2d) -> "FusedMaxPool2d":
+        k, s, p = (m.kernel_size, m.stride, m.padding)
+        if not all(isinstance(v, int) for v in (k, s, p)) or m.dilation not in (1, (1, 1)) or m.ceil_mode or m.return_indices:
+            raise ValueError("FusedMaxPool2d: square window, int stride/padding, no dilation / ceil mode / indices")
+        return cls(k, s, p)
+
+
 def _basic_forward(self, x):
     identity = x if self.downsample is None else self.downsample(x)
     out = self.bn1(self.conv1(x))
@@ -157,7 +206,8 @@ def fuse_backbone(model: nn.Module) -> int:
     """Rewire a torchvision ResNet so each BN runs as a fused post-pass.
 
     Stem ``bn1 -> relu`` and the block tails ``bn -> (+identity) -> relu`` fuse;
-    downsample BNs stay plain (no activation).  Returns the number of fused BNs.
+    downsample BNs stay plain (no activation); the stem max-pool runs on the
+    native pool kernels.  Returns the number of fused BNs.
     """
     from torchvision.models.resnet import BasicBlock, Bottleneck, ResNet
 
@@ -174,6 +224,8 @@ def fuse_backbone(model: nn.Module) -> int:
         if isinstance(m, ResNet) or getattr(m, "_canvas_stem", False):
             swap(m, "bn1", True)
             m.relu = nn.Identity()
+            if isinstance(getattr(m, "maxpool", None), nn.MaxPool2d) and not isinstance(m.maxpool, FusedMaxPool2d):
+                m.maxpool = FusedMaxPool2d.from_pool(m.maxpool)
         elif isinstance(m, BasicBlock):
             swap(m, "bn1", True)
             swap(m, "bn2", True)

@@ -93,7 +93,7 @@ class _RefBN(nn.BatchNorm2d):
 
 
 def _swap_ref(model):
-    from paper_2304_07741_b200.post import FusedBatchNorm2d
+    from paper_2304_07741_b200.post import FusedBatchNorm2d, FusedMaxPool2d
 
     for name, parent in list(model.named_modules()):
         for cname, child in list(parent.named_children()):
@@ -101,6 +101,8 @@ def _swap_ref(model):
                 setattr(parent, cname, _RefConv(child))
             elif isinstance(child, FusedBatchNorm2d):
                 setattr(parent, cname, _RefBN(child))
+            elif isinstance(child, FusedMaxPool2d):
+                setattr(parent, cname, nn.MaxPool2d(child.kernel_size, child.stride, child.padding))
             elif isinstance(child, nn.Sequential):
                 for i, sub in enumerate(child):
                     if isinstance(sub, FusedBatchNorm2d):

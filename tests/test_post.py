@@ -1,6 +1,7 @@
 """BN post-pass (include/canvas_post.h): exports, the ResNet
 rewiring, and GPU parity of the fused kernels against torch fp64 BatchNorm
-(+ residual, + ReLU) — forward, backward and the running-stat update."""
+(+ residual, + ReLU) — forward, backward and the running-stat update — and of
+the native stem max-pool against torch (ties on ReLU zeros, NaN)."""
 
 import copy
 import re
@@ -20,7 +21,7 @@ RTOL, ATOL = 1e-4, 1e-5  # north star fp32 tolerance vs fp64
 def test_exports_every_declared_symbol():
     lib = post.load_library()
     names = sorted(set(re.findall(r"^\w[\w\s\*]*?\b(canvas_\w+)\(", HDR.read_text(), re.M)))
-    assert len(names) == 5, names
+    assert len(names) == 7, names
     for n in names:
         assert hasattr(lib, n), n
     assert lib.canvas_post_abi_version() == post.ABI_VERSION
@@ -139,3 +140,30 @@ def test_fused_resnet_training_step_matches_unfused():
         assert n0 == n1
         err = (p1.grad.double() - p0.grad).norm() / max(p0.grad.norm(), 1e-30)
         assert err < 1e-3, (n0, float(err))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,k,s,p", [((4, 8, 112, 112), 3, 2, 1), ((2, 3, 9, 7), 3, 2, 1), ((2, 4, 8, 8), 2, 2, 0), ((1, 2, 11, 10), 3, 1, 1)])
+def test_maxpool_parity(shape, k, s, p):
+    dev = torch.device("cuda:0")
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(shape, generator=g)
+    x = torch.relu(x)  # ReLU zeros: exact ties in many windows (first maximum wins)
+    dy = torch.randn(F.max_pool2d(x, k, s, p).shape, generator=g)
+    xr = x.double().requires_grad_(True)
+    yr = F.max_pool2d(xr, k, s, p)
+    yr.backward(dy.double())
+    m = post.FusedMaxPool2d(k, s, p)
+    xg = x.to(dev).requires_grad_(True)
+    y = m(xg)
+    y.backward(dy.to(dev))
+    assert torch.equal(y.cpu().double(), yr.detach())
+    torch.testing.assert_close(xg.grad.cpu().double(), xr.grad, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.gpu
+def test_maxpool_nan_propagates():
+    x = torch.zeros(1, 1, 4, 4, device="cuda")
+    x[0, 0, 3, 3] = float("nan")  # only window (1, 1) covers it
+    y = post.FusedMaxPool2d(3, 2, 1)(x)
+    assert torch.isnan(y[0, 0, 1, 1]) and not torch.isnan(y[0, 0, :1]).any() and not torch.isnan(y[0, 0, 1, 0])
