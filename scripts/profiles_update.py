@@ -46,9 +46,14 @@ def main():
     h, data = rows[hi], rows[hi + 1 :]
     # drop the warm-up steps (cuDNN autotuner trials) — keep the last 3 steps' launches
     per_step = int(os.environ.get("LAUNCHES_PER_STEP", "0"))
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     if per_step:
         data = data[-3 * per_step :]
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    elif os.environ.get("STEP_MARKER"):  # "<kernel name>:<launches per step>": keep the last 3 steps
+        name, cnt = os.environ["STEP_MARKER"].rsplit(":", 1)
+        pos = [i for i, r in enumerate(data) if r[ki] == name]
+        if len(pos) >= 3 * int(cnt):
+            data = data[pos[len(pos) - 3 * int(cnt)] :]
     agg = collections.defaultdict(lambda: [0, 0.0])
     tot = canvas = 0.0
     for r in data:
@@ -60,7 +65,7 @@ def main():
         agg[re.sub(r"^k\d+_", "", r[ki])[:90]][1] += v
     with open(os.path.join(out, f"{tag}_launches_summary.txt"), "w") as f:
         f.write("ncu --metrics gpu__time_duration.sum --clock-control none -- python bench.py --steps 1 --warmup 3 --no-cpu --no-context\n")
-        f.write("(cold-cache, serialised per-launch times; warm-up steps dropped, last timed + 2 e2e steps kept: compare SHARES, not absolutes)\n")
+        f.write("(cold-cache, serialised per-launch times of the CUDA-graph kernel nodes; warm-up steps dropped, last timed + 2 e2e steps kept: compare SHARES, not absolutes)\n")
         f.write(f"total {tot / 1e6:.1f} ms over {len(data)} launches; Canvas kernels {100 * canvas / tot:.1f}% of device time\n\n")
         for k, (n, v) in sorted(agg.items(), key=lambda x: -x[1][1])[:45]:
             f.write(f"{100 * v / tot:6.2f}% {n:5d} launches {v / n / 1e3:9.1f} us/launch  {k}\n")
