@@ -57,6 +57,7 @@ PLANES_CTAS = int(os.environ.get("CANVAS_PLANES_CTAS", str(148 * 64)))  # CTAs o
 GEMM_TILE = 64
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
+WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
 TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
@@ -1221,7 +1222,7 @@ class Lowerer:
         small = M <= 16
         use_tc = self.use_tc and J >= 32 and not small
         if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
-            jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()))
+            jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()), WGRAD_SMALL_JT_MAX)
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
         else:
             if use_tc:  # >= ~6 CTAs per SM at batch 256 without going below 512 pixels per partial
@@ -1261,7 +1262,7 @@ class Lowerer:
             grid = (GridRule(0, J, 128), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
             self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
         elif small:
-            jt = 1 << max(0, (256 // M).bit_length() - 1)
+            jt = min(1 << max(0, (256 // M).bit_length() - 1), WGRAD_SMALL_JT_MAX)
             jt = min(jt, 1 << (J - 1).bit_length()) if J > 1 else 1
             functor = functor[: functor.rindex("};")] + f"  static constexpr int JT = {jt};\n}};\n"
             launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::wgrad_small<{name}_F>(a); }}\n'

@@ -104,3 +104,32 @@ def test_operand_writeback(cin, cout, stride, monkeypatch):
     executor._plan_cached.cache_clear()
     assert "SAVE_B = true" in case.plan.source
     assert_close(case, *emu_run(case), f"write-back {cin}->{cout} s{stride}")
+
+
+def _nvcc_plan(i):
+    import shutil
+    import subprocess
+    import tempfile
+
+    from paper_2304_07741_b200.executor import plan_for
+
+    texts = ["canvas-ir v1\n" + t for t in open("tests/golden/sampler_10_7_256.cir").read().split("canvas-ir v1\n")[1:]]
+    p = plan_for(texts[i], c_in=64, c_out=64, h=56, w=56, k=3, g=4)
+    d = tempfile.mkdtemp()
+    try:
+        with open(f"{d}/p.cu", "w") as f:
+            f.write(p.source)
+        r = subprocess.run([os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"), "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-cubin", "-I", "paper_2304_07741_b200/csrc/kernels", "-diag-suppress", "177", f"{d}/p.cu", "-o", f"{d}/p.cubin"], capture_output=True, text=True)
+        return None if r.returncode == 0 else f"#{i}: " + " | ".join(l for l in r.stderr.splitlines() if "error" in l)[:300]
+    finally:
+        shutil.rmtree(d, ignore_errors=True)
+
+
+@pytest.mark.skipif(not os.path.exists(os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")), reason="nvcc not present")
+def test_sweep_256_plans_compile_for_sm100a():
+    """Every kernel of the 256-kernel sweep lowers at config-1 shapes (C=64,
+    56x56) to code ptxas accepts for sm_100a (shared-memory limits, register
+    budgets) — the build check the GPU's NVRTC would otherwise fail at run time."""
+    with ProcessPoolExecutor(min(16, os.cpu_count() or 1), mp_context=multiprocessing.get_context("spawn")) as ex:
+        errs = [e for e in ex.map(_nvcc_plan, range(256)) if e]
+    assert not errs, errs[:5]
