@@ -33,6 +33,7 @@ from __future__ import annotations
 
 import math
 import os
+import re
 import struct
 from dataclasses import dataclass, field
 
@@ -40,6 +41,7 @@ from .graph import VIEW_OPS, ConcreteGraph, LoweringError
 
 ABI_VERSION = 1
 BLOB_MAGIC = b"CNVSBLOB"
+_IDENT = re.compile(r"[A-Za-z_]\w*")
 MAX_KSLOTS = 24  # pointers per kernel argument block (csrc/kernels/canvas_kernels.cuh)
 
 # fixed global slots; weights / grads / saved / workspace follow (see Plan.slot_*)
@@ -277,6 +279,11 @@ class Fn:
         # flat index r = q * S + s is split into a block-uniform plane q and a
         # per-thread spatial s (pointwise_planes)
         self.planes: tuple | None = None
+        # warp-/block-uniform index variables (seeded by the caller: "k" rows of a
+        # tcgen05 producer, "q"/"n" of a plane-major functor).  Offsets are emitted
+        # as (per-lane part) + (uniform part) so the uniform part is shared by all
+        # lanes and the per-lane part by all rows: one IMAD.WIDE per gathered element
+        self.uniform: set = set()
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -320,6 +327,8 @@ class Fn:
         v = self.fresh("i")
         self.emit(f"const int {v} = {expr};")
         self.memo_put(("i", expr), v)
+        if self.uniform and all(t in self.uniform for t in _IDENT.findall(expr)):
+            self.uniform.add(v)
         return v
 
     def fvar(self, expr: str, key=None) -> str:
@@ -358,7 +367,7 @@ class Fn:
         self.bases[key] = r
         return r
 
-    def offset(self, d: TDesc, coords) -> str:
+    def _offset_terms(self, d: TDesc, coords):
         """Element offset sum(coord_i * stride_i) as an affine form over base
         coordinates, with every run of coordinates that came from decomposing a
         flat index (over contiguous strides) folded back into that index — e.g.
@@ -388,10 +397,29 @@ class Fn:
                     del acc[v]
                 acc[sub] = acc.get(sub, 0) + alpha
                 break
-        terms = [f"{v}" if k == 1 else f"{v}*{k}" for v, k in sorted(acc.items(), key=lambda kv: -abs(kv[1])) if k]
-        if const:
-            terms.append(f"({const})")
-        return self.ivar(" + ".join(terms) if terms else "0")
+        return acc, const
+
+    def offset_parts(self, d: TDesc, coords) -> tuple[str, str]:
+        """(per-lane part, uniform part) of the element offset, each an int var or "0"."""
+        acc, const = self._offset_terms(d, coords)
+
+        def join(items, c=0):
+            terms = [f"{v}" if k == 1 else f"{v}*{k}" for v, k in sorted(items, key=lambda kv: -abs(kv[1])) if k]
+            if c:
+                terms.append(f"({c})")
+            return self.ivar(" + ".join(terms) if terms else "0")
+
+        uni = [(v, k) for v, k in acc.items() if v in self.uniform]
+        lane = [(v, k) for v, k in acc.items() if v not in self.uniform]
+        if not self.uniform or not uni:
+            return join(lane, const), "0"
+        return join(lane), join(uni, const)
+
+    def offset(self, d: TDesc, coords) -> str:
+        lane, uni = self.offset_parts(d, coords)
+        if uni == "0":
+            return lane
+        return uni if lane == "0" else self.ivar(f"{lane} + {uni}")
 
     def suffix(self, flat: str, m: int) -> str:
         """``flat % m``; in a plane-major functor r % m = s % m whenever m | S."""
@@ -400,9 +428,17 @@ class Fn:
         return self.ivar(f"{flat} % {m}")
 
     def addr(self, d: TDesc, coords) -> str:
-        off = self.offset(d, coords)
+        lane, uni = self.offset_parts(d, coords)
         p, nb = self.base(d)
-        return f"{p} + ({nb} + {off})" if nb else f"{p} + {off}"
+        if nb and "n" in self.uniform:  # image base is uniform too (plane-major functors)
+            uni = nb if uni == "0" else self.ivar(f"{nb} + {uni}")
+        elif nb:
+            lane = nb if lane == "0" else self.ivar(f"{nb} + {lane}")
+        if uni == "0":
+            return f"{p} + {lane}"
+        if lane == "0":
+            return f"{p} + {uni}"
+        return f"{p} + {lane} + {uni}"  # (p + lane) shared across rows, + uniform per row
 
     def raw_ivar(self, expr: str) -> str:
         v = self.ivar(expr)
@@ -478,6 +514,9 @@ class Fn:
         return coords
 
     def flatten(self, coords, ext) -> str:
+        got = self.flat_of.get(tuple(coords))
+        if got is not None and got[1] == tuple(ext):
+            return got[0]  # recomposing a decomposed flat index: it is that index
         expr = None
         for c, e in zip(coords, ext):
             expr = c if expr is None else f"({expr})*{e} + {c}"
@@ -1129,11 +1168,13 @@ class Lowerer:
         fb.pre = []
         fb.computing = None
         fb.local_slots = fa.local_slots  # share the pointer table
+        fb.uniform = {"k"}  # tcgen05 producers: k-row per warp, lane = pixel
         bval = bfn(fb)
         fs = Fn(self)
         fs.pre = []
         fs.computing = None
         fs.local_slots = fa.local_slots
+        fs.uniform = {"m"}  # TMEM epilogue: column per iteration, lane = pixel
         sfn(fs, "acc")
         lines = [
             f"struct {name}_F {{",
@@ -1157,6 +1198,7 @@ class Lowerer:
             fv.pre = []
             fv.computing = None
             fv.local_slots = fa.local_slots
+            fv.uniform = {"k"}
             save(fv)
             lines += ["  static constexpr bool SAVE_B = true;", "  static __device__ __forceinline__ void save_b(const CanvasArgs& a, const long long n, const int k, const int s, const float val) {"]
             lines += ["    " + s for s in fv.pre] + fv.lines + ["  }"]
@@ -1237,6 +1279,7 @@ class Lowerer:
         fa.pre, fb.pre = [], []
         fa.computing = fb.computing = None
         fb.local_slots = fa.local_slots
+        fa.uniform, fb.uniform = {"m"}, {"k"}  # tcgen05 wgrad producers: row per warp, lane = pixel
         aval = afn(fa)
         bval = bfn(fb)
         pslot_local = fa.ptr(-1 - k_ws)  # partials (fixed up to the real ws slot in finish())
