@@ -416,6 +416,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, cv_u32 byte
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// warm L2 with the 128 B line at p (the producers' upcoming gathers)
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -646,6 +650,16 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         const long long tc = t < T ? t : T - 1;
         pn[mb] = (int)(tc / F::S);
         ps[mb] = (int)(tc - (long long)pn[mb] * F::S);
+      }
+      // warm L2 with every source row of this CTA's 128-pixel tile (4 lines per row)
+      if constexpr (F::NPF > 0) {
+        for (int i = threadIdx.x; i < F::NPF * 4; i += PW * 32) {
+          const long long t = t0 + (i & 3) * 32;
+          if (t < T) {
+            const long long n = t / F::S;
+            prefetch_l2(F::pf_addr(a, n, (int)(t - n * F::S), i >> 2));
+          }
+        }
       }
       constexpr int ROWS = kBK / PW;
       float va[ROWS][4];
@@ -1098,6 +1112,20 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       }
     };
     const int off_l = ((lane >> 2) << 4) | ((lane & 3) << 2);  // chunk/word of this pixel before the swizzle
+    // warm L2 with the source rows of k-block kb (one 128 B line per row):
+    // issued kPfDist k-blocks before the gathers of that k-block
+    constexpr int kPfDist = 3;
+    auto prefetch = [&](int kb) {
+      if constexpr (F::NPF > 0) {
+        const long long t = tbeg + (long long)kb * kBK;
+        if (kb < KB && t < tend) {
+          const long long n = t / F::S;
+          const int s = (int)(t - n * F::S);
+          for (int i = threadIdx.x; i < F::NPF; i += PW * 32) prefetch_l2(F::pf_addr(a, n, s, i));
+        }
+      }
+    };
+    for (int d = 1; d <= kPfDist; ++d) prefetch(d);
     if (KB > 0) gather(0);
     for (int kb = 0; kb < KB; ++kb) {
       const int st = kb % STAGES;
@@ -1128,6 +1156,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       }
       fence_async_smem();
       mbar_arrive(&full[st]);
+      prefetch(kb + 1 + kPfDist);
       if (kb + 1 < KB) gather(kb + 1);
     }
     mbar_wait(done, 0);

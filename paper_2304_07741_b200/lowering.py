@@ -70,7 +70,8 @@ TC_PERSIST = os.environ.get("CANVAS_TC_PERSIST", "1") == "1"  # persistent fwd/d
 TC_PW = int(os.environ.get("CANVAS_TC_PW", "8"))  # producer warps of the persistent GEMM
 SMS = 148
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
-TC_WGRAD_TCHUNK = 4096
+L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
+TC_WGRAD_TCHUNK = int(os.environ.get("CANVAS_WGRAD_TCHUNK", "4096"))  # max pixels per wgrad partial
 TC_WGRAD_PW = int(os.environ.get("CANVAS_WGRAD_PW", "16"))  # wgrad producer warps
 TC_PIX_PW = int(os.environ.get("CANVAS_PIX_PW", "0"))  # 0 = auto  # fwd/dgrad (non-persistent) producer warps  # pixels per wgrad split (128 k-blocks of 32)
 
@@ -284,6 +285,7 @@ class Fn:
         # as (per-lane part) + (uniform part) so the uniform part is shared by all
         # lanes and the per-lane part by all rows: one IMAD.WIDE per gathered element
         self.uniform: set = set()
+        self.loaded: dict = {}  # (slot, image stride) -> TDesc of every tensor this functor reads
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -480,6 +482,7 @@ class Fn:
         return v, True
 
     def load(self, d: TDesc, coords, preds: tuple = ()) -> str:
+        self.loaded.setdefault((d.slot, d.bstride), d)
         # the guard only protects addresses built from raw (possibly out-of-range)
         # coordinates; an all-in-range load is safe and stays unpredicated so the
         # compiler can share it
@@ -1160,6 +1163,33 @@ class Lowerer:
             else:
                 self.p.saved[sidx] = SizeRule(0, 1, 0)  # path without operand write-back: no buffer
 
+    @staticmethod
+    def prefetch_members(f: Fn, fns, S: int) -> list:
+        """``NPF`` / ``pf_addr``: one 128 B line per row of every materialised
+        tensor the producer functors ``fns`` read, at pixel (n, s) — the
+        producers warm L2 with the rows of upcoming k-blocks / of their pixel
+        tile, so the gathers hit L2 instead of waiting on DRAM.  A tensor with
+        an image stride that is a multiple of S is treated as [rows][S]; every
+        address stays inside its image, so a mismatch only wastes a prefetch."""
+        rows = []
+        seen = set()
+        for g in fns:
+            for key, d in g.loaded.items():
+                if key in seen:
+                    continue
+                seen.add(key)
+                if d.bstride % S == 0 and d.bstride // S >= 1:
+                    rows.append((f.ptr(d.slot), d.bstride, d.bstride // S))
+        if not L2_PREFETCH or not rows:
+            return ["  static constexpr int NPF = 0;", "  static __device__ __forceinline__ const float* pf_addr(const CanvasArgs&, const long long, const int, const int) { return nullptr; }"]
+        body = ["  static __device__ __forceinline__ const float* pf_addr(const CanvasArgs& a, const long long n, const int s, int i) {"]
+        for ptr, bs, r in rows:
+            body.append(f"    if (i < {r}) return {ptr} + n * {bs}LL + (long long)i * {S} + s;")
+            body.append(f"    i -= {r};")
+        body.append("    return nullptr;")
+        body.append("  }")
+        return [f"  static constexpr int NPF = {sum(r for _, _, r in rows)};"] + body
+
     def emit_gemm_nk(self, name, fa: Fn, a_expr: str, bfn, sfn, M, K, S, phase, beta, what, nbytes, flops, save=None) -> bool:
         """C[n][m][s] = sum_k A(m,k) * B(n,k,s) through canvas::gemm_nk (one shared slot table).
         ``save(f)``: emit the store of B's value ``val`` at (n, k, s) — the operand
@@ -1204,6 +1234,7 @@ class Lowerer:
             lines += ["    " + s for s in fv.pre] + fv.lines + ["  }"]
         else:
             lines += ["  static constexpr bool SAVE_B = false;", "  static __device__ __forceinline__ void save_b(const CanvasArgs&, const long long, const int, const int, const float) {}"]
+        lines += self.prefetch_members(fa, [fb], S)
         lines += ["};"]
         functor = "\n".join(lines) + "\n"
         if tc:
@@ -1292,6 +1323,7 @@ class Lowerer:
         lines += ["  static __device__ __forceinline__ float B(const CanvasArgs& a, const long long n, const int k, const int s) {"]
         lines += ["    " + s for s in fb.pre] + fb.lines + [f"    return {bval};", "  }"]
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
+        lines += self.prefetch_members(fa, [fb, fa], S)
         lines += ["};"]
         functor = "\n".join(lines) + "\n"
         if use_tc:
