@@ -114,3 +114,20 @@ def test_wide_channels(name, cin, cout, hw, stride):
     case = reference(zoo.ALL[name], cin, cout, hw, hw, stride=stride, n=2)
     y, dx, dws = run_gpu(case)
     assert_close(case, y, dx, dws, f"{name} {cin}->{cout} {hw}^2 s{stride}")
+
+
+@pytest.mark.parametrize("golden,count", [("sampler_16_7_64.cir", 64), ("sampler_20_0_16.cir", 16)])
+def test_larger_sampled_kernels(golden, count):
+    """Every kernel of the reference's nodes=16 (64 kernels) and nodes=20 (16
+    kernels) sweeps, through the C ABI vs the fp64 oracle at a small shape with
+    Fig.-2 replication (C_in=16 -> C_out=32, stride 2)."""
+    texts = _sweep(f"tests/golden/{golden}")
+    assert len(texts) == count
+    bad = []
+    for i, t in enumerate(texts):
+        case = reference(t, 16, 32, 10, 9, stride=2, n=2)
+        try:
+            assert_close(case, *run_gpu(case), f"{golden} #{i}")
+        except AssertionError as e:
+            bad.append(str(e)[:200])
+    assert not bad, bad[:5]
