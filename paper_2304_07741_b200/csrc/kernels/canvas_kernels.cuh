@@ -38,6 +38,15 @@ struct CanvasArgs {
 
 namespace canvas {
 
+// p + off as one mad.wide (32-bit signed offset scaled to the 64-bit pointer):
+// opaque to the compiler, so a per-lane base pointer shared by many rows is not
+// re-associated into per-element 32-bit adds + sign-extended 64-bit math
+__device__ __forceinline__ float* ptr_add(float* p, int off) {
+  float* r;
+  asm("mad.wide.s32 %0, %1, 4, %2;" : "=l"(r) : "r"(off), "l"(p));
+  return r;
+}
+
 // warp index of this thread, through a shuffle so the compiler can prove it
 // warp-uniform: the warp-role branches of the tcgen05 templates then stay
 // uniform and producer index math / memory descriptors live on the uniform
@@ -553,6 +562,49 @@ struct Smem {
   static constexpr int BYTES = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;  // + alignment slack
 };
 
+// Shared memory plan of the wgrad pipeline with JG row tiles of 128 per CTA:
+// STAGES x {A_hi[JG], A_lo[JG], B_hi, B_lo} + barriers.
+template <int NT, int JG, int STAGES>
+struct SmemW {
+  static constexpr int A_TILE = kBM * 128;
+  static constexpr int A_BYTES = JG * A_TILE;
+  static constexpr int B_BYTES = NT * 128;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE;
+  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;
+};
+
+// wgrad MMA issuer: per k-block, JG row tiles x 4 K=8 steps x 3 MMAs, tile g
+// accumulating into TMEM columns [g*NT, (g+1)*NT)
+template <int NT, int JG, int STAGES>
+__device__ __forceinline__ void mma_loop_w(uint8_t* smem, cv_u64* full, cv_u64* empty, cv_u64* done, cv_u32 tmem, int KB) {
+  using L = SmemW<NT, JG, STAGES>;
+  constexpr cv_u32 idesc = idesc_tf32(NT, false);
+  for (int kb = 0; kb < KB; ++kb) {
+    const int st = kb % STAGES;
+    mbar_wait(&full[st], (kb / STAGES) & 1);
+    fence_after();
+    const cv_u32 base = smem_u32(smem + st * L::STAGE);
+    const cv_u32 b_hi = base + 2 * L::A_BYTES;
+    const cv_u32 b_lo = b_hi + L::B_BYTES;
+#pragma unroll
+    for (int g = 0; g < JG; ++g) {
+      const cv_u32 a_hi = base + g * L::A_TILE;
+      const cv_u32 a_lo = a_hi + L::A_BYTES;
+      const cv_u32 d = tmem + g * NT;
+#pragma unroll
+      for (int kk = 0; kk < kBK / 8; ++kk) {
+        const cv_u32 o = kk * 32;
+        mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_hi + o), idesc, !(kb == 0 && kk == 0));
+        mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_lo + o), idesc, 1);
+        mma_tf32(d, desc_k_sw128(a_lo + o), desc_k_sw128(b_hi + o), idesc, 1);
+      }
+    }
+    commit(&empty[st]);
+  }
+  commit(done);
+}
+
 // MMA issuer: consumes STAGES-deep ring, 3 MMAs per K=8 step (hi.hi, hi.lo, lo.hi)
 // NACC > 1: the K loop is split into NACC contiguous chunks accumulated in
 // separate TMEM regions (tmem + i*NT) and summed by the epilogue in fp32: the
@@ -1051,11 +1103,14 @@ __device__ __forceinline__ void tc_pack_b(const CanvasArgs& a) {
 // m (operand A), reduction over a TCHUNK slice of pixels t; partials are
 // summed in order by reduce_partials (deterministic).
 // ---------------------------------------------------------------------------
-template <class F, int NT, int STAGES, int PW = tc::kProducerWarps>
+// JG > 1: each CTA owns JG row tiles of 128 input channels (TMEM columns
+// JG*NT), so the A operand (output-channel gradients, NT rows) is gathered once
+// per JG tiles instead of once per tile.
+template <class F, int NT, int STAGES, int PW = tc::kProducerWarps, int JG = 1>
 __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   using namespace tc;
-  using L = Smem<NT, STAGES>;
-  constexpr int NCOLS = TmemCols<NT>::value;
+  using L = SmemW<NT, JG, STAGES>;
+  constexpr int NCOLS = TmemCols<NT * JG>::value;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem(smem_raw);
   cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
@@ -1082,14 +1137,14 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   const long long tbeg = (long long)blockIdx.z * F::TCHUNK;
   const long long tend = tbeg + F::TCHUNK < T ? tbeg + F::TCHUNK : T;
   const int KB = (int)((tend - tbeg + kBK - 1) / kBK);
-  const int j0 = blockIdx.x * kBM;  // rows: input channels
-  const int m0 = blockIdx.y * NT;   // cols: output channels
+  const int j0 = blockIdx.x * kBM * JG;  // rows: input channels (JG tiles of 128)
+  const int m0 = blockIdx.y * NT;        // cols: output channels
 
   if (warp < PW) {
     // lane = pixel of the 32-pixel k-block (coalesced gathers, one pixel
     // decomposition per k-block); warp w owns rows w, w+8, ... (channel index
     // math is warp-uniform); each warp writes whole 128 B swizzled rows.
-    constexpr int RA = kBM / PW, RB = (NT + PW - 1) / PW;
+    constexpr int RA = kBM * JG / PW, RB = (NT + PW - 1) / PW;
     float va[RA], vb[RB];
     auto gather = [&](int kb) {
       const long long t = tbeg + (long long)kb * kBK + lane;
@@ -1136,7 +1191,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       uint8_t* sb_lo = sb_hi + L::B_BYTES;
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
-        const int row = warp + PW * w;
+        const int row = warp + PW * w;  // tile row >> 7, row & 127 inside it (tiles are contiguous)
         const int off = row * 128 + (off_l ^ ((row & 7) << 4));
         float h, l;
         split_tf32(va[w], h, l);
@@ -1162,13 +1217,14 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     mbar_wait(done, 0);
     fence_after();
     const int q = warp & 3;
-    const int jj = j0 + q * 32 + lane;
     float* P = F::partials(a) + (long long)blockIdx.z * F::M * F::J;
-    constexpr int HALF = ((NT + 31) / 32) * 16;
-    const int cbeg = (warp >> 2) * HALF;
-    for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {
+    // (tile, 16-column chunk) units over the PW/4 warpgroups; warp quadrant q reads TMEM lanes q*32..
+    constexpr int CH = (NT + 15) / 16;
+    for (int u = warp >> 2; u < JG * CH; u += PW / 4) {
+      const int g = u / CH, cc = (u - g * CH) * 16;
+      const int jj = j0 + g * kBM + q * 32 + lane;
       float v[16];
-      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + cc, v);
+      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + g * NT + cc, v);
       if (jj < F::J) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -1178,7 +1234,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       }
     }
   } else if (warp == PW && lane == 0) {
-    if (KB > 0) mma_loop<NT, STAGES>(smem, full, empty, done, tmem, KB);
+    if (KB > 0) mma_loop_w<NT, JG, STAGES>(smem, full, empty, done, tmem, KB);
     else tc::mbar_arrive(done);
   }
   fence_before();

@@ -71,6 +71,7 @@ TC_PW = int(os.environ.get("CANVAS_TC_PW", "8"))  # producer warps of the persis
 SMS = 148
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
+TC_WGRAD_JG_MAX = int(os.environ.get("CANVAS_WGRAD_JG", "2"))  # max row tiles per wgrad CTA
 TC_WGRAD_TCHUNK = int(os.environ.get("CANVAS_WGRAD_TCHUNK", "4096"))  # max pixels per wgrad partial
 TC_WGRAD_PW = int(os.environ.get("CANVAS_WGRAD_PW", "16"))  # wgrad producer warps
 TC_PIX_PW = int(os.environ.get("CANVAS_PIX_PW", "0"))  # 0 = auto  # fwd/dgrad (non-persistent) producer warps  # pixels per wgrad split (128 k-blocks of 32)
@@ -85,6 +86,24 @@ def tc_tile(cols: int, ntmax: int | None = None) -> tuple[int, int, int]:
         return nt, nct, 2
     stages = max(2, min(4, TC_SMEM_BUDGET // stage))
     return nt, nct, stages
+
+
+def wgrad_smem_bytes(nt: int, jg: int, stages: int) -> int:
+    """Must match canvas::tc::SmemW<NT, JG, STAGES>::BYTES."""
+    return stages * (2 * jg * 128 * 128 + 2 * nt * 128) + (2 * stages + 1) * 8 + 16 + 1024
+
+
+def wgrad_jg(J: int, nt: int) -> int:
+    """Row tiles of 128 input channels per wgrad CTA: the output-channel operand
+    (nt rows) is gathered once per group, so group as many tiles as TMEM
+    (jg*nt <= 512 columns) and a 2-stage ring in 220 KB of smem allow."""
+    jg = 1
+    if nt < 128:  # measured: at NT = 64 (layer1) grouping is slower (fewer, longer CTAs)
+        return 1
+    for cand in range(2, TC_WGRAD_JG_MAX + 1):
+        if cand * nt <= 512 and wgrad_smem_bytes(nt, cand, 2) <= 220 * 1024 and J > 128 * (cand - 1):
+            jg = cand
+    return jg
 
 
 def tc_persist_cfg(nt: int) -> tuple[int, int]:
@@ -440,7 +459,15 @@ class Fn:
             return f"{p} + {lane}"
         if lane == "0":
             return f"{p} + {uni}"
-        return f"{p} + {lane} + {uni}"  # (p + lane) shared across rows, + uniform per row
+        # 64-bit lane pointer (shared by every row of the producer) + per-row 32-bit
+        # uniform offset: one IMAD.WIDE per gathered element
+        key = ("lp", p, lane)
+        lp = self.memo_get(key)
+        if not lp:
+            lp = self.fresh("lp")
+            self.emit(f"float* const {lp} = {p} + {lane};")
+            self.memo_put(key, lp)
+        return f"canvas::ptr_add({lp}, {uni})"
 
     def raw_ivar(self, expr: str) -> str:
         v = self.ivar(expr)
@@ -1299,7 +1326,7 @@ class Lowerer:
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
         else:
             if use_tc:  # >= ~6 CTAs per SM at batch 256 without going below 512 pixels per partial
-                tiles = -(-J // 128) * tc_tile(M)[1]
+                tiles = -(-J // (128 * wgrad_jg(J, tc_tile(M)[0]))) * tc_tile(M)[1]
                 z = -(-(6 * SMS) // tiles)
                 tchunk = min(TC_WGRAD_TCHUNK, max(512, -(-(-(-(256 * S) // z)) // 128) * 128))
             else:
@@ -1328,13 +1355,18 @@ class Lowerer:
         functor = "\n".join(lines) + "\n"
         if use_tc:
             nt, nct, stages = tc_tile(M)
-            smem = tc_smem_bytes(nt, stages)
+            jg = wgrad_jg(J, nt)
+            if jg > 1:
+                stages = 2
+                smem = wgrad_smem_bytes(nt, jg, stages)
+            else:
+                smem = tc_smem_bytes(nt, stages)
             pw = TC_WGRAD_PW
             threads = (pw + 2) * 32
             pair = smem <= TC_SMEM_PAIR and pw <= 8
-            launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}, {pw}>(a); }}\n'
+            launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}, {pw}, {jg}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
-            grid = (GridRule(0, J, 128), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
+            grid = (GridRule(0, J, 128 * jg), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
             self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
         elif small:
             jt = min(1 << max(0, (256 // M).bit_length() - 1), WGRAD_SMALL_JT_MAX)

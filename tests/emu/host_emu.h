@@ -31,6 +31,7 @@ struct CanvasArgs {
 };
 
 namespace canvas {
+inline float* ptr_add(float* p, int off) { return p + off; }
 template <class F, int V = 1>
 void pointwise(const CanvasArgs& a) {
   for (long long n = 0; n < a.n; ++n)
@@ -127,6 +128,6 @@ template <class F, int NT>
 void tc_pack_b(const CanvasArgs&) {}
 template <class F, int NT, int STAGES, int PW, int EW>
 void tc_gemm_pix_persistent(const CanvasArgs& a) { gemm_nk<F>(a); }
-template <class F, int NT, int STAGES, int PW = 8>
+template <class F, int NT, int STAGES, int PW = 8, int JG = 1>
 void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 }  // namespace canvas
