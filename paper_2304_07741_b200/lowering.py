@@ -1134,6 +1134,28 @@ class Lowerer:
         wslot, _ = self.fc_weight_slot(u)
         io = 4 * (nu.numel + self._input_numel(nu))
         flops = 2 * O * K * S
+        if O <= SMALL_FC and nu.sp_ext and len(nu.ext) == len(nu.sp_ext) + 1 and math.prod(nu.sp_ext) >= 512:
+            # few outputs (fc(G), fc(1), ...): one thread per pixel computes all O
+            # outputs in one pass over the K inputs (the input is read once, not O
+            # times); needs enough pixels to fill the GPU (H*W >= 512 per image:
+            # at 7x7 the per-output mapping is faster, measured 0.049 vs 0.084 ms)
+            def body(f, u=u):
+                sp = tuple(f.decompose("r", nu.sp_ext))
+                accs = [f.fresh("acc") for _ in range(O)]
+                f.emit("float " + ", ".join(f"{a_} = 0.f" for a_ in accs) + ";")
+                i = f.fresh("i")
+                f.loop(i, K)
+                ch = tuple(f.decompose(i, nv.ch_ext))
+                x = self.val(f, v, ch + sp)
+                for o, a_ in enumerate(accs):
+                    f.emit(f"{a_} = fmaf(__ldg({f.ptr(wslot)} + {o * K} + {i}), {x}, {a_});")
+                f.close()
+                for o, a_ in enumerate(accs):
+                    for d, b in targets:
+                        f.store(d, (str(o),) + sp, a_, b)
+
+            self.launch_pointwise(name, math.prod(nu.sp_ext), body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1)
+            return
         if min(O, K) <= SMALL_FC:
 
             def body(f, u=u):
