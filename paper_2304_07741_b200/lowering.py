@@ -60,6 +60,7 @@ GEMM_TILE = 64
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
+INLINE_SMALL_DGRAD = os.environ.get("CANVAS_INLINE_SMALL_DGRAD", "1") == "1"  # few-output FC dgrad inlined into the gradient sum
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
 TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
@@ -573,6 +574,7 @@ class Lowerer:
         self.count_desc: dict[int, TDesc] = {}
         self.grad_desc: dict[int, TDesc] = {}
         self.dgrad_desc: dict[int, TDesc] = {}  # FC node u -> contribution buffer for its input
+        self.inline_dgrad: set = set()  # few-output FCs whose input-gradient contribution is evaluated inline
         self.dot_desc: dict[int, TDesc] = {}  # softmax node u -> row dot buffer
         self.computing_grad = None
 
@@ -822,6 +824,16 @@ class Lowerer:
             dot = f.load(d, rc)
             return f.fvar(f"{y} * ({g} - {dot})")
         if op == "fc":
+            if u in self.inline_dgrad:
+                # few-output FC: its input-gradient contribution sum_o W[o, i] g_u[o, s]
+                # is an O-term dot evaluated where the gradient sum needs it
+                O, K = self.g.fc_shape(u)
+                wslot, _ = self.fc_weight_slot(u)
+                nv = self.nodes[v]
+                i = f.flatten(coords[: nv.nch], nv.ch_ext)
+                sp = coords[nv.nch :]
+                terms = [f.fvar(f"__ldg({f.ptr(wslot)} + {o * K} + {i}) * {self.grad(f, u, (str(o),) + tuple(sp))}") for o in range(O)]
+                return f.fvar(" + ".join(terms))
             return f.load(self.dgrad_desc[u], coords)
         if op == "bcast":
             return self.bcast_contrib(f, nu, pos, v, coords)
@@ -1442,6 +1454,8 @@ class Lowerer:
                     _, d = self._new_ws(nv.ext)
                     self.dgrad_desc[u] = d
                     self.grad_desc[v] = d
+            elif INLINE_SMALL_DGRAD and self.g.fc_shape(u)[0] <= SMALL_FC and len(self.nodes[u].ext) == len(self.nodes[u].sp_ext) + 1:
+                self.inline_dgrad.add(u)  # consumers of v evaluate this FC's contribution inline
             else:
                 _, d = self._new_ws(nv.ext)
                 self.dgrad_desc[u] = d
@@ -1525,6 +1539,9 @@ class Lowerer:
         O, K = self.g.fc_shape(u)
         S = math.prod(nu.sp_ext)
         wslot, dwslot = self.fc_weight_slot(u)
+        if u in self.inline_dgrad:
+            self.lower_fc_wgrad(u)
+            return
         dd = self.dgrad_desc[u]
         beta = dx_beta if dd.slot == SLOT_DX else BETA_NONE
         flops = 2 * O * K * S
@@ -1561,7 +1578,17 @@ class Lowerer:
                 f.store(dd, c, val, beta != BETA_NONE)
 
             self.emit_gemm_nk(name, fa, a_expr, bfn, sfn, M=K, K=O, S=S, phase=1, beta=beta, what=f"dgrad {K}x{O}x{S} n{u}->n{v}", nbytes=4 * (nu.numel + nv.numel), flops=flops)
-        # wgrad: dW[o,i] = sum_{n,s} dL/du[n,o,s] * v[n,i,s]
+        self.lower_fc_wgrad(u)
+
+    def lower_fc_wgrad(self, u: int) -> None:
+        """dW[o,i] = sum_{n,s} dL/du[n,o,s] * v[n,i,s]."""
+        nu = self.nodes[u]
+        v = nu.ins[0]
+        nv = self.nodes[v]
+        O, K = self.g.fc_shape(u)
+        S = math.prod(nu.sp_ext)
+        _, dwslot = self.fc_weight_slot(u)
+        flops = 2 * O * K * S
         name = f"k{len(self.p.kernel_names)}_bwd_wgrad{u}"
 
         def afn(f):

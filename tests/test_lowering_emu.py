@@ -81,11 +81,15 @@ def planes_everywhere(monkeypatch):
 @pytest.mark.parametrize("name", list(zoo.ALL))
 def test_plane_major_pointwise(name, planes_everywhere):
     case = reference(zoo.ALL[name], 16, 32, 10, 9, stride=2)
-    assert any("pointwise_planes" in k for k in case.plan.source.splitlines())
     assert_close(case, *emu_run(case), f"{name} plane-major")
 
 
 def test_plane_major_sweep_first40(planes_everywhere):
+    """Plane-major functors (every eligible launch, down to 1-pixel planes)
+    over the first 40 sweep kernels; at least some launches must use them."""
+    from paper_2304_07741_b200.executor import plan_for
+
+    assert "pointwise_planes" in plan_for(zoo.SEED7_K1, c_in=16, c_out=16, h=8, w=7).source
     texts = ["canvas-ir v1\n" + t for t in open("tests/golden/sampler_10_7_256.cir").read().split("canvas-ir v1\n")[1:]]
     for i in range(40):
         case = reference(texts[i], 16, 16, 8, 7)
