@@ -118,16 +118,32 @@ __device__ __forceinline__ void softmax_rows(const CanvasArgs& a) {
     const bool ok = row < total;
     const long long n = ok ? row / F::ROWS : 0;
     const int r = ok ? (int)(row - n * F::ROWS) : 0;
+    // a thread's slice of the row (PT values) stays in registers when short, so
+    // the row is read from memory once
+    constexpr int PT = (F::SPAN + SL - 1) / SL;
+    constexpr bool REG = PT <= 64;
+    float xv[REG ? PT : 1];
     float m = -INFINITY, s = 0.f;
+    auto online = [&](float x) {
+      if (x > m) {
+        s = s * expf(m - x) + 1.f;
+        m = x;
+      } else {
+        s += expf(x - m);
+      }
+    };
     if (ok) {
-      for (int j = sl; j < F::SPAN; j += SL) {
-        const float x = F::in(a, n, r, j);
-        if (x > m) {
-          s = s * expf(m - x) + 1.f;
-          m = x;
-        } else {
-          s += expf(x - m);
+      if constexpr (REG) {
+#pragma unroll
+        for (int q = 0; q < PT; ++q) {
+          const int j = sl + q * SL;
+          if (j < F::SPAN) {
+            xv[q] = F::in(a, n, r, j);
+            online(xv[q]);
+          }
         }
+      } else {
+        for (int j = sl; j < F::SPAN; j += SL) online(F::in(a, n, r, j));
       }
     }
     red[sl][tr] = m;
@@ -142,8 +158,17 @@ __device__ __forceinline__ void softmax_rows(const CanvasArgs& a) {
 #pragma unroll
     for (int i = 0; i < SL; ++i) S += red[i][tr];
     __syncthreads();
-    if (ok)
-      for (int j = sl; j < F::SPAN; j += SL) F::out(a, n, r, j, expf(F::in(a, n, r, j) - M) / S);
+    if (ok) {
+      if constexpr (REG) {
+#pragma unroll
+        for (int q = 0; q < PT; ++q) {
+          const int j = sl + q * SL;
+          if (j < F::SPAN) F::out(a, n, r, j, expf(xv[q] - M) / S);
+        }
+      } else {
+        for (int j = sl; j < F::SPAN; j += SL) F::out(a, n, r, j, expf(F::in(a, n, r, j) - M) / S);
+      }
+    }
   }
 }
 

@@ -61,6 +61,7 @@ MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
 INLINE_SMALL_DGRAD = os.environ.get("CANVAS_INLINE_SMALL_DGRAD", "1") == "1"  # few-output FC dgrad inlined into the gradient sum
+SOFTMAX_REG_SPAN = int(os.environ.get("CANVAS_SOFTMAX_REG_SPAN", "64"))  # softmax rows up to this long are held in registers
 SMALL_FC = 16  # min(out, K) at or below which an FC is a per-pixel SIMT dot (K4 fc_small)
 TC_THREADS = 320  # tcgen05 GEMM: 8 producer/epilogue warps + MMA warp + bulk-copy warp
 TC_SMEM_BUDGET = 200 * 1024
@@ -1074,6 +1075,35 @@ class Lowerer:
             stmt_fn(c, x)
             f.close()
 
+        if S <= SOFTMAX_REG_SPAN:
+            # short rows: evaluate the input once into registers (fully unrolled), so
+            # the row is read from memory once instead of three times
+            xs = f.fresh("xs")
+            f.emit(f"float {xs}[{S}];")
+
+            def uloop(stmt_fn):
+                j = f.fresh("j")
+                f.emit("#pragma unroll")
+                f.open(f"for (int {j} = 0; {j} < {S}; ++{j})")
+                stmt_fn(j)
+                f.close()
+
+            def first(j):
+                c = pc + tuple(f.decompose(j, span)) + qc
+                f.emit(f"{xs}[{j}] = {self.val(f, nd.ins[0], c)};")
+                f.emit(f"{mx} = fmaxf({mx}, {xs}[{j}]);")
+
+            uloop(first)
+            uloop(lambda j: f.emit(f"{sm} += expf({xs}[{j}] - {mx});"))
+
+            def write_r(j):
+                c = pc + tuple(f.decompose(j, span)) + qc
+                y = f.fvar(f"expf({xs}[{j}] - {mx}) / {sm}")
+                for d, beta in targets:
+                    f.store(d, c, y, beta)
+
+            uloop(write_r)
+            return
         loop(lambda c, x: f.emit(f"{mx} = fmaxf({mx}, {x});"))
         loop(lambda c, x: f.emit(f"{sm} += expf({x} - {mx});"))
 
