@@ -334,36 +334,63 @@ __device__ __forceinline__ void gemm_wgrad(const CanvasArgs& a) {
 // ---------------------------------------------------------------------------
 template <class F>
 __device__ __forceinline__ void wgrad_small(const CanvasArgs& a) {
+  // thread (j = tid % JT, pixel group pg = tid / JT) accumulates all M outputs of
+  // row j over the tile pixels q = pg (mod PG): per pixel one Bs read, one
+  // (vector) As read of the M gradients and M FMAs; the PG partial sums are
+  // combined in a fixed order at the end (deterministic)
   constexpr int TP = 64;
   constexpr int JT = F::JT;
-  __shared__ float As[F::M][TP + 1];
+  constexpr int PG = 256 / JT;
+  constexpr int M = F::M;
+  constexpr int MP = (M + 3) / 4 * 4;
+  __shared__ __align__(16) float As[TP][MP];
   __shared__ float Bs[JT][TP + 1];
+  __shared__ float red[PG > 1 ? PG : 1][M][JT];
   const long long T = a.n * (long long)F::S;
   const long long tbeg = (long long)blockIdx.z * F::TCHUNK;
   const long long tend = tbeg + F::TCHUNK < T ? tbeg + F::TCHUNK : T;
   const int j0 = blockIdx.x * JT;
   const int tid = threadIdx.x;
-  const int om = tid / JT, oj = tid % JT;  // output owned by this thread (tid < M*JT)
-  float acc = 0.f;
+  const int oj = tid % JT, pg = tid / JT;
+  float acc[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) acc[m] = 0.f;
   for (long long t0 = tbeg; t0 < tend; t0 += TP) {
     const int p = tid % TP;
     const long long t = t0 + p;
     const bool ok = t < tend;
     const long long n = ok ? t / F::S : 0;
     const int s = ok ? (int)(t - n * F::S) : 0;
-    for (int r = tid / TP; r < F::M; r += blockDim.x / TP) As[r][p] = ok ? F::A(a, n, r, s) : 0.f;
+    for (int r = tid / TP; r < MP; r += blockDim.x / TP) As[p][r] = (ok && r < M) ? F::A(a, n, r < M ? r : 0, s) : 0.f;
     for (int r = tid / TP; r < JT; r += blockDim.x / TP) {
       const int j = j0 + r;
       Bs[r][p] = (ok && j < F::J) ? F::B(a, n, j, s) : 0.f;
     }
     __syncthreads();
-    if (om < F::M) {
-#pragma unroll 8
-      for (int q = 0; q < TP; ++q) acc = fmaf(As[om][q], Bs[oj][q], acc);
+#pragma unroll 4
+    for (int q = pg; q < TP; q += PG) {
+      const float b = Bs[oj][q];
+#pragma unroll
+      for (int m4 = 0; m4 < MP; m4 += 4) {
+        const float4 av = *reinterpret_cast<const float4*>(&As[q][m4]);
+        if (m4 + 0 < M) acc[m4 + 0] = fmaf(av.x, b, acc[m4 + 0]);
+        if (m4 + 1 < M) acc[m4 + 1] = fmaf(av.y, b, acc[m4 + 1]);
+        if (m4 + 2 < M) acc[m4 + 2] = fmaf(av.z, b, acc[m4 + 2]);
+        if (m4 + 3 < M) acc[m4 + 3] = fmaf(av.w, b, acc[m4 + 3]);
+      }
     }
     __syncthreads();
   }
-  if (om < F::M && j0 + oj < F::J) F::partials(a)[((long long)blockIdx.z * F::M + om) * F::J + j0 + oj] = acc;
+#pragma unroll
+  for (int m = 0; m < M; ++m) red[PG > 1 ? pg : 0][m][oj] = acc[m];
+  __syncthreads();
+  for (int o = tid; o < M * JT; o += blockDim.x) {
+    const int m = o / JT, jj = o % JT;
+    float v = 0.f;
+#pragma unroll
+    for (int g = 0; g < PG; ++g) v += red[g][m][jj];
+    if (j0 + jj < F::J) F::partials(a)[((long long)blockIdx.z * M + m) * F::J + j0 + jj] = v;
+  }
 }
 
 template <class F>
