@@ -463,6 +463,13 @@ def main() -> None:
                 tr = json.load(f).get(args.kernel, {}).get(roofline["kernel"].split("_", 1)[1])
             if tr and tr.get("batch") == args.batch:
                 roofline["traffic"] = tr["dram_bytes"]
+                if tr.get("warp_instructions") and clk.get("sm_mhz"):
+                    # the computed-operand GEMMs are bound by SIMT operand production,
+                    # so the SM issue rate (4 warp-instructions / clock / SM) is the
+                    # roofline that binds them: ncu instruction count of one launch over
+                    # its live duration, against 148 SMs x 4 x the measured SM clock
+                    ips = tr["warp_instructions"] / (roofline["launch_ms"] * 1e-3)
+                    roofline["issue"] = {"achieved_warp_inst_per_s": round(ips / 1e9, 1), "peak_warp_inst_per_s": round(148 * 4 * clk["sm_mhz"] * 1e6 / 1e9, 1), "unit": "G warp-instructions/s", "frac": round(ips / (148 * 4 * clk["sm_mhz"] * 1e6), 3), "source": tr.get("source")}
         except (OSError, ValueError):
             pass
 

@@ -39,7 +39,8 @@ def main():
     for k, d in s.items():
         rd = float(d.get("dram__bytes_read.sum", "0 byte").split()[0]) * _unit(d.get("dram__bytes_read.sum", "0 byte"))
         wr = float(d.get("dram__bytes_write.sum", "0 byte").split()[0]) * _unit(d.get("dram__bytes_write.sum", "0 byte"))
-        traffic.setdefault("seed7_k1", {})[k.split("_", 1)[1]] = {"batch": 256, "dram_bytes": int(rd + wr), "source": f"profiles/{tag}_ncu_full.json"}
+        inst = d.get("Executed Instructions", "0 inst").split()[0].replace(",", "")
+        traffic.setdefault("seed7_k1", {})[k.split("_", 1)[1]] = {"batch": 256, "dram_bytes": int(rd + wr), "warp_instructions": int(float(inst)), "source": f"profiles/{tag}_ncu_full.json"}
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     rows = list(csv.reader(open(launches)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
