@@ -309,6 +309,9 @@ def main() -> None:
 
     per_step_launches += 4 * sum(isinstance(m, FusedBatchNorm2d) for m in core.modules())  # stats+apply, reduce+apply
     per_step_launches += 2 * sum(isinstance(m, FusedMaxPool2d) for m in core.modules())  # fwd, bwd
+    from paper_2304_07741_b200.dense_conv import TcConv2d
+
+    per_step_launches += 4 * sum(isinstance(m, TcConv2d) for m in core.modules())  # pack, fwd, wgrad, reduce
 
     # --- CUDA graph of the whole step (forward, backward, all-reduce, SGD): one
     # replay per step, so host launch overhead leaves the critical path.  The

@@ -579,6 +579,19 @@ class Lowerer:
         self.dot_desc: dict[int, TDesc] = {}  # softmax node u -> row dot buffer
         self.computing_grad = None
 
+    @classmethod
+    def bare(cls, plan: Plan, use_tc: bool = True) -> "Lowerer":
+        """A Lowerer without a kernel graph: the kernel emitters (GEMM templates
+        with caller-written functor bodies) for dense layers (dense_conv.py)."""
+        lw = cls.__new__(cls)
+        lw.use_tc, lw.g, lw.p, lw.nodes, lw.out = use_tc, None, plan, [], None
+        lw.kernels = []
+        lw.fwd_mat, lw.grad_mat = set(), set()
+        lw.fwd_desc, lw.count_desc, lw.grad_desc, lw.dgrad_desc, lw.dot_desc = {}, {}, {}, {}, {}
+        lw.inline_dgrad = set()
+        lw.computing_grad = None
+        return lw
+
     # -------------------------------------------------------------- materialisation
     def replicated_pointwise(self) -> set:
         """Pointwise nodes worth one extra HBM round trip: those whose inline

@@ -93,6 +93,7 @@ class _RefBN(nn.BatchNorm2d):
 
 
 def _swap_ref(model):
+    from paper_2304_07741_b200.dense_conv import TcConv2d
     from paper_2304_07741_b200.post import FusedBatchNorm2d, FusedMaxPool2d
 
     for name, parent in list(model.named_modules()):
@@ -103,6 +104,10 @@ def _swap_ref(model):
                 setattr(parent, cname, _RefBN(child))
             elif isinstance(child, FusedMaxPool2d):
                 setattr(parent, cname, nn.MaxPool2d(child.kernel_size, child.stride, child.padding))
+            elif isinstance(child, TcConv2d):
+                plain = nn.Conv2d(child.in_channels, child.out_channels, child.kernel_size, child.stride, child.padding, bias=False)
+                plain.load_state_dict(child.state_dict())
+                setattr(parent, cname, plain)
             elif isinstance(child, nn.Sequential):
                 for i, sub in enumerate(child):
                     if isinstance(sub, FusedBatchNorm2d):
@@ -166,8 +171,7 @@ def test_network_parity(name):
                 caps[lname] = {"x": i[0].detach().clone()}
                 o.register_hook(lambda g, lname=lname: caps[lname].__setitem__("dy", g.detach().clone()))
             mod.register_forward_hook(fwd)
-    xg = x.clone().requires_grad_(True)
-    out = m(xg)
+    out = m(x.clone())  # parameters require grad, so every layer output does
     out.backward(torch.randn(out.shape, generator=torch.Generator().manual_seed(1)).to(dev))
     from oracle import torch_ref as R
     from paper_2304_07741_b200.executor import solve_target

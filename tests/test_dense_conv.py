@@ -1,0 +1,57 @@
+"""Dense (backbone) convolution on the tcgen05 GEMM templates (dense_conv.py):
+plan construction on CPU; GPU parity of the forward and the weight gradient
+against the fp64 oracle (F.conv2d) at the ResNet stem geometry."""
+
+import pytest
+import torch
+import torch.nn.functional as F
+from torch import nn
+
+from paper_2304_07741_b200 import dense_conv
+
+RTOL, ATOL = 1e-4, 1e-5
+
+
+def test_stem_plan_lowers():
+    p = dense_conv.lower_conv2d(3, 64, 7, 2, 3, 224, 224)
+    names = [L.name for L in p.launches]
+    assert any(n.endswith("fwd_conv") for n in names) and any("wgrad_conv" in n for n in names)
+    assert "tc_gemm" in p.source and p.blob()[:8] == b"CNVSBLOB"
+
+
+def test_cpu_path_is_torch():
+    torch.manual_seed(0)
+    c = nn.Conv2d(3, 8, 7, 2, 3, bias=False)
+    t = dense_conv.TcConv2d.from_conv(c)
+    x = torch.randn(2, 3, 20, 18)
+    assert torch.equal(t(x), c(x))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,h,w", [(2, 224, 224), (3, 37, 29)])
+def test_stem_conv_parity(n, h, w):
+    torch.backends.cudnn.allow_tf32 = False
+    g = torch.Generator().manual_seed(0)
+    x = torch.randn(n, 3, h, w, generator=g)
+    c = nn.Conv2d(3, 64, 7, 2, 3, bias=False)
+    with torch.no_grad():
+        c.weight.copy_(torch.randn(c.weight.shape, generator=g) / 12)
+    dyshape = F.conv2d(x, c.weight, stride=2, padding=3).shape
+    dy = torch.randn(dyshape, generator=g)
+    wr = c.weight.detach().double().requires_grad_(True)
+    yr = F.conv2d(x.double(), wr, stride=2, padding=3)
+    yr.backward(dy.double())
+    t = dense_conv.TcConv2d.from_conv(c).cuda()
+    y = t(x.cuda())
+    y.backward(dy.cuda())
+    torch.testing.assert_close(y.cpu().double(), yr.detach(), rtol=RTOL, atol=ATOL)
+    err = (t.weight.grad.cpu().double() - wr.grad).abs().max() / (ATOL + RTOL * wr.grad.abs().max())
+    assert err <= 1.0, float(err)
+
+
+@pytest.mark.gpu
+def test_input_gradient_refused():
+    t = dense_conv.TcConv2d(3, 8, 7, 2, 3, bias=False).cuda()
+    x = torch.randn(1, 3, 16, 16, device="cuda", requires_grad=True)
+    with pytest.raises(NotImplementedError):
+        t(x).sum().backward()
