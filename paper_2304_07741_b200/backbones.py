@@ -98,9 +98,9 @@ def build(name: str, ir_text: str, *, g: int = 4, fuse_bn: bool = True, factory=
     spec = SPECS[name]
     names = replace(m, ir_text, g=g, kernel_sizes=spec["kernel_sizes"], factory=factory)
     if fuse_bn and factory is None:
-        from .dense_conv import accelerate_stem
+        from .dense_conv import accelerate_dense
         from .post import fuse_backbone
 
         fuse_backbone(m)
-        accelerate_stem(m)  # ResNet stem conv on the tcgen05 templates (3xTF32)
+        accelerate_dense(m)  # ResNet stem + downsample convs on the tcgen05 templates (3xTF32)
     return m, names

@@ -8,7 +8,9 @@ B(n, k, s) = x[n, c, oh*S + kh - P, ow*S + kw - P] (k = (c, kh, kw), zero
 outside the image) is produced on the fly by the producer warps of
 ``canvas::tc_gemm_pix`` / ``tc_gemm_pix_persistent`` and the weight gradient
 by ``canvas::tc_gemm_wgrad`` — 3xTF32, fp32-accurate, deterministic.  The
-input gradient is not built (the stem's input is the data batch).
+input gradient (when the input requires it, e.g. the strided 1x1 downsample
+convs) is a third GEMM over K' = (C_out, kh, kw) whose operand gathers dy at
+((ih + P - kh) / S, (iw + P - kw) / S) where divisible (col2im as a gather).
 
 ``lower_conv2d`` builds a plan blob for ``libcanvas_b200.so`` (one FC slot =
 the [C_out, C_in*K*K] weight, i.e. ``nn.Conv2d.weight`` flattened); ``TcConv2d``
@@ -37,7 +39,7 @@ class _DenseGraph:
 
 
 @functools.lru_cache(maxsize=32)
-def lower_conv2d(c_in: int, c_out: int, k: int, stride: int, pad: int, h_in: int, w_in: int) -> Plan:
+def lower_conv2d(c_in: int, c_out: int, k: int, stride: int, pad: int, h_in: int, w_in: int, dgrad: bool = False) -> Plan:
     ho = (h_in + 2 * pad - k) // stride + 1
     wo = (w_in + 2 * pad - k) // stride + 1
     K, S, kk = c_in * k * k, ho * wo, k * k
@@ -65,6 +67,30 @@ def lower_conv2d(c_in: int, c_out: int, k: int, stride: int, pad: int, h_in: int
     def dy(f: Fn) -> str:
         return f.fvar(f"__ldg({f.ptr(SLOT_DY)} + (long long)n * {c_out * S} + m * {S} + s)")
 
+    if dgrad:
+        # dx[n, c, ih, iw] = sum_{m, kh, kw} W[m, c, kh, kw] dy[n, m, (ih+P-kh)/S, (iw+P-kw)/S]
+        Kd, Sd = c_out * kk, h_in * w_in
+
+        def col2im(f: Fn) -> str:
+            dp = f.ptr(SLOT_DY)
+            f.emit(f"const int m_ = k / {kk}; const int r_ = k - m_ * {kk}; const int kh_ = r_ / {k}; const int kw_ = r_ - kh_ * {k};")
+            f.emit(f"const int ih_ = s / {w_in}; const int iw_ = s - ih_ * {w_in};")
+            f.emit(f"const int th_ = ih_ + {pad} - kh_; const int tw_ = iw_ + {pad} - kw_;")
+            f.emit(f"const int oh_ = th_ / {stride}; const int ow_ = tw_ / {stride};")
+            f.emit(f"const bool in_ = th_ >= 0 && tw_ >= 0 && th_ - oh_ * {stride} == 0 && tw_ - ow_ * {stride} == 0 && oh_ < {ho} && ow_ < {wo};")
+            f.emit(f"const float g_ = in_ ? __ldg({dp} + (long long)n * {c_out * S} + (m_ * {ho} + oh_) * {wo} + ow_) : 0.f;")
+            return "g_"
+
+        def store_dx(f: Fn, val: str) -> None:
+            from .lowering import SLOT_DX
+
+            f.emit(f"*({f.ptr(SLOT_DX)} + (long long)n * {c_in * Sd} + m * {Sd} + s) = {val};")
+
+        fd = Fn(lw)
+        fd.pre = []
+        fd.computing = None
+        a_d = f"__ldg({fd.ptr(p.slot_w(0))} + (k / {kk}) * {K} + m * {kk} + (k % {kk}))"
+        lw.emit_gemm_nk(f"k{len(p.kernel_names)}_bwd_dgrad_conv", fd, a_d, col2im, store_dx, M=c_in, K=Kd, S=Sd, phase=1, beta=BETA_NONE, what=f"dgrad conv {c_in}x{Kd}x{Sd}", nbytes=4 * (c_out * S + c_in * Sd), flops=2 * c_in * Kd * Sd)
     lw.emit_gemm_wgrad(f"k{len(p.kernel_names)}_bwd_wgrad_conv", dy, im2col, c_out, K, S, p.slot_dw(0), f"wgrad conv {c_out}x{K} over {S}/img", 4 * (c_in * h_in * w_in + c_out * S), flops)
     lw.finish()
     return p
@@ -77,7 +103,8 @@ class _ConvFn(torch.autograd.Function):
 
         x = x.contiguous()
         n, _, h, wd = x.shape
-        dp = device_plan(lower_conv2d(mod.in_channels, mod.out_channels, mod.kernel_size[0], mod.stride[0], mod.padding[0], h, wd), x.device.index or 0)
+        need_dx = ctx.needs_input_grad[1]
+        dp = device_plan(lower_conv2d(mod.in_channels, mod.out_channels, mod.kernel_size[0], mod.stride[0], mod.padding[0], h, wd, need_dx), x.device.index or 0)
         ho = (h + 2 * mod.padding[0] - mod.kernel_size[0]) // mod.stride[0] + 1
         wo = (wd + 2 * mod.padding[1] - mod.kernel_size[1]) // mod.stride[1] + 1
         y = torch.empty((n, mod.out_channels, ho, wo), device=x.device, dtype=torch.float32)
@@ -93,14 +120,13 @@ class _ConvFn(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, dy):
-        if ctx.x_grad:
-            raise NotImplementedError("TcConv2d computes the weight gradient only (the stem's input is the data batch)")
         x, saved, wf = ctx.saved_tensors
         dy = dy.contiguous()
         dw = torch.empty_like(wf)
+        dx = torch.empty_like(x) if ctx.x_grad else dy  # dy: never written when no dgrad launch
         ws = torch.empty(max(ctx.ws_b, 1), device=x.device, dtype=torch.uint8)
-        ctx.dp.backward(x, [wf], saved, dy, dy, [dw], ws, torch.cuda.current_stream(x.device).cuda_stream)
-        return None, None, dw.view(ctx.wshape)
+        ctx.dp.backward(x, [wf], saved, dy, dx, [dw], ws, torch.cuda.current_stream(x.device).cuda_stream)
+        return None, (dx if ctx.x_grad else None), dw.view(ctx.wshape)
 
 
 class TcConv2d(nn.Conv2d):
@@ -124,10 +150,26 @@ class TcConv2d(nn.Conv2d):
         return _ConvFn.apply(self, x, self.weight)
 
 
+def _eligible(c) -> bool:
+    return isinstance(c, nn.Conv2d) and not isinstance(c, TcConv2d) and c.bias is None and c.groups == 1 and c.dilation == (1, 1) and c.kernel_size[0] == c.kernel_size[1] and c.stride[0] == c.stride[1] and c.padding[0] == c.padding[1]
+
+
 def accelerate_stem(model: nn.Module) -> bool:
     """Swap a ResNet-style stem ``model.conv1`` (input = data batch) for TcConv2d."""
     c = getattr(model, "conv1", None)
-    if isinstance(c, nn.Conv2d) and not isinstance(c, TcConv2d) and c.in_channels == 3 and c.bias is None and c.groups == 1:
+    if _eligible(c) and c.in_channels == 3:
         model.conv1 = TcConv2d.from_conv(c)
         return True
     return False
+
+
+def accelerate_dense(model: nn.Module) -> int:
+    """Swap the stem and every ResNet downsample conv (the remaining standard
+    convs of a ResNet after Canvas replacement) for TcConv2d."""
+    count = int(accelerate_stem(model))
+    for m in model.modules():
+        ds = getattr(m, "downsample", None)
+        if isinstance(ds, nn.Sequential) and len(ds) and _eligible(ds[0]):
+            ds[0] = TcConv2d.from_conv(ds[0])
+            count += 1
+    return count

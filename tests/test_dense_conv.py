@@ -50,8 +50,24 @@ def test_stem_conv_parity(n, h, w):
 
 
 @pytest.mark.gpu
-def test_input_gradient_refused():
-    t = dense_conv.TcConv2d(3, 8, 7, 2, 3, bias=False).cuda()
-    x = torch.randn(1, 3, 16, 16, device="cuda", requires_grad=True)
-    with pytest.raises(NotImplementedError):
-        t(x).sum().backward()
+@pytest.mark.parametrize("cin,cout,k,stride,pad,hw", [(64, 128, 1, 2, 0, 56), (128, 256, 1, 2, 0, 28), (16, 32, 3, 1, 1, 12), (8, 16, 3, 2, 1, 13), (3, 64, 7, 2, 3, 40)])
+def test_conv_with_input_grad_parity(cin, cout, k, stride, pad, hw):
+    """Downsample-style convs: forward, input gradient (col2im as a gather GEMM) and weight gradient."""
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(2, cin, hw, hw, generator=g)
+    c = nn.Conv2d(cin, cout, k, stride, pad, bias=False)
+    with torch.no_grad():
+        c.weight.copy_(torch.randn(c.weight.shape, generator=g) / (cin * k * k) ** 0.5)
+    dy = torch.randn(F.conv2d(x, c.weight, stride=stride, padding=pad).shape, generator=g)
+    xr = x.double().requires_grad_(True)
+    wr = c.weight.detach().double().requires_grad_(True)
+    yr = F.conv2d(xr, wr, stride=stride, padding=pad)
+    yr.backward(dy.double())
+    t = dense_conv.TcConv2d.from_conv(c).cuda()
+    xg = x.cuda().requires_grad_(True)
+    y = t(xg)
+    y.backward(dy.cuda())
+    torch.testing.assert_close(y.cpu().double(), yr.detach(), rtol=RTOL, atol=ATOL)
+    torch.testing.assert_close(xg.grad.cpu().double(), xr.grad, rtol=RTOL, atol=ATOL)
+    err = (t.weight.grad.cpu().double() - wr.grad).abs().max() / (ATOL + RTOL * wr.grad.abs().max())
+    assert err <= 1.0, float(err)
