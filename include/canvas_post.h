@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define CANVAS_POST_ABI_VERSION 1
+#define CANVAS_POST_ABI_VERSION 2
 #define CANVAS_POST_OK 0
 #define CANVAS_POST_ERR_ARGS (-5)
 #define CANVAS_POST_ERR_CUDA (-4)
@@ -41,19 +41,21 @@ size_t canvas_bn_workspace(int64_t N, int64_t C, int64_t HW);
 
 /* y = act(bn(x) [+ residual]); act = ReLU when relu != 0.  running_mean /
  * running_var may both be NULL (no running-stat update).  Writes the batch
- * mean and 1/sqrt(var + eps) to save_mean / save_invstd for the backward. */
+ * mean and 1/sqrt(var + eps) to save_mean / save_invstd for the backward, and,
+ * when relu_mask is non-NULL (relu != 0), one byte (y > 0) per element. */
 int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const float* residual, float* y,
                       const float* gamma, const float* beta, float* running_mean, float* running_var,
-                      float* save_mean, float* save_invstd, float momentum, float eps, int relu, void* workspace,
-                      void* stream);
+                      float* save_mean, float* save_invstd, float momentum, float eps, int relu, uint8_t* relu_mask,
+                      void* workspace, void* stream);
 
 /* dx (and dresidual = the gradient reaching the residual, when non-NULL),
- * dgamma, dbeta (written, not accumulated) from dy = dL/dy.  y is the
- * forward output, used as the ReLU mask (relu'(0) = 0); may be NULL when
- * relu == 0. */
-int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const float* dy,
-                       const float* gamma, const float* save_mean, const float* save_invstd, float* dx,
-                       float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace, void* stream);
+ * dgamma, dbeta (written, not accumulated) from dy = dL/dy.  The ReLU mask
+ * (relu'(0) = 0) comes from relu_mask (the forward's bytes) when non-NULL,
+ * else from y > 0 (the forward output); both may be NULL when relu == 0. */
+int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const uint8_t* relu_mask,
+                       const float* dy, const float* gamma, const float* save_mean, const float* save_invstd,
+                       float* dx, float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace,
+                       void* stream);
 
 /* Max-pool (square window K, stride S, padding P, no dilation, floor mode) of
  * [N, C, H, W]: y [N, C, OH, OW] and the winner's window slot (kh*K + kw, one

@@ -139,6 +139,7 @@ struct FwdArgs {
   const double2* part;
   float momentum, eps;
   int relu;
+  uint8_t* mask;  // nullable: ReLU mask bytes (y > 0) for the backward
 };
 
 template <int V>
@@ -195,11 +196,13 @@ __global__ void __launch_bounds__(kBlock) bn_apply(Geo g, FwdArgs a) {
         o.w = fmaxf(o.w, 0.f);
       }
       st4(a.y + off, o);
+      if (a.mask) *reinterpret_cast<uchar4*>(a.mask + off) = make_uchar4(o.x > 0.f, o.y > 0.f, o.z > 0.f, o.w > 0.f);
     } else {
       float o = fmaf(__ldg(a.x + off) - mean, sc, bt);
       if (r) o += __ldg(r + off);
       if (relu) o = fmaxf(o, 0.f);
       a.y[off] = o;
+      if (a.mask) a.mask[off] = o > 0.f;
     }
   });
 }
@@ -218,6 +221,7 @@ struct BwdArgs {
   float* dbeta;
   double2* part;
   int relu;
+  const uint8_t* mask;  // nullable: ReLU mask bytes written by the forward (read instead of y)
 };
 
 template <int V>
@@ -229,7 +233,13 @@ __global__ void __launch_bounds__(kBlock) bn_bwd_reduce(Geo g, BwdArgs a) {
   for_units<V>(g, c, p, [&](long long off) {
     if (V == 4) {
       float4 d = ld4(a.dy + off);
-      if (relu) {
+      if (relu && a.mask) {
+        const uchar4 m = __ldg(reinterpret_cast<const uchar4*>(a.mask + off));
+        d.x = m.x ? d.x : 0.f;
+        d.y = m.y ? d.y : 0.f;
+        d.z = m.z ? d.z : 0.f;
+        d.w = m.w ? d.w : 0.f;
+      } else if (relu) {
         const float4 m = ld4(a.y + off);
         d.x = m.x > 0.f ? d.x : 0.f;
         d.y = m.y > 0.f ? d.y : 0.f;
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kBlock) bn_bwd_reduce(Geo g, BwdArgs a) {
       sgx = fmaf(d.x, (v.x - mean) * inv, fmaf(d.y, (v.y - mean) * inv, fmaf(d.z, (v.z - mean) * inv, fmaf(d.w, (v.w - mean) * inv, sgx))));
     } else {
       float d = __ldg(a.dy + off);
-      if (relu && !(__ldg(a.y + off) > 0.f)) d = 0.f;
+      if (relu && !(a.mask ? __ldg(a.mask + off) != 0 : __ldg(a.y + off) > 0.f)) d = 0.f;
       sg += d;
       sgx = fmaf(d, (__ldg(a.x + off) - mean) * inv, sgx);
     }
@@ -279,7 +289,13 @@ __global__ void __launch_bounds__(kBlock) bn_bwd_apply(Geo g, BwdArgs a) {
   for_units<V>(g, c, p, [&](long long off) {
     if (V == 4) {
       float4 d = ld4(a.dy + off);
-      if (relu) {
+      if (relu && a.mask) {
+        const uchar4 m = __ldg(reinterpret_cast<const uchar4*>(a.mask + off));
+        d.x = m.x ? d.x : 0.f;
+        d.y = m.y ? d.y : 0.f;
+        d.z = m.z ? d.z : 0.f;
+        d.w = m.w ? d.w : 0.f;
+      } else if (relu) {
         const float4 m = ld4(a.y + off);
         d.x = m.x > 0.f ? d.x : 0.f;
         d.y = m.y > 0.f ? d.y : 0.f;
@@ -296,7 +312,7 @@ __global__ void __launch_bounds__(kBlock) bn_bwd_apply(Geo g, BwdArgs a) {
       if (dr) st4(dr + off, d);
     } else {
       float d = __ldg(a.dy + off);
-      if (relu && !(__ldg(a.y + off) > 0.f)) d = 0.f;
+      if (relu && !(a.mask ? __ldg(a.mask + off) != 0 : __ldg(a.y + off) > 0.f)) d = 0.f;
       a.dx[off] = k * (d - mg - (__ldg(a.x + off) - mean) * inv * mgx);
       if (dr) dr[off] = d;
     }
@@ -463,8 +479,8 @@ size_t canvas_bn_workspace(int64_t N, int64_t C, int64_t HW) {
 
 int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const float* residual, float* y,
                       const float* gamma, const float* beta, float* running_mean, float* running_var,
-                      float* save_mean, float* save_invstd, float momentum, float eps, int relu, void* workspace,
-                      void* stream) {
+                      float* save_mean, float* save_invstd, float momentum, float eps, int relu, uint8_t* relu_mask,
+                      void* workspace, void* stream) {
   if (N < 1 || C < 1 || HW < 1 || !x || !y || !gamma || !beta || !save_mean || !save_invstd || !workspace ||
       (running_mean == nullptr) != (running_var == nullptr) || N * C * HW >= (1LL << 40)) {
     snprintf(g_err, sizeof g_err, "canvas_bn_forward: bad arguments");
@@ -473,7 +489,7 @@ int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const fl
   Geo g = make_geo((int)N, (int)C, (int)HW, slices((int)N, (int)C));
   if (!aligned16(x) || !aligned16(residual) || !aligned16(y)) g.V = 1, g.U = g.HW;
   cudaStream_t s = (cudaStream_t)stream;
-  FwdArgs a{x, residual, y, gamma, beta, running_mean, running_var, save_mean, save_invstd, (const double2*)workspace, momentum, eps, relu};
+  FwdArgs a{x, residual, y, gamma, beta, running_mean, running_var, save_mean, save_invstd, (const double2*)workspace, momentum, eps, relu, relu ? relu_mask : nullptr};
   const dim3 grid(g.P, g.C);
   if (g.V == 4) {
     bn_stats<4><<<grid, kBlock, 0, s>>>(g, x, (double2*)workspace);
@@ -486,18 +502,19 @@ int canvas_bn_forward(int64_t N, int64_t C, int64_t HW, const float* x, const fl
   return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_bn_forward launch", e);
 }
 
-int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const float* dy,
-                       const float* gamma, const float* save_mean, const float* save_invstd, float* dx,
-                       float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace, void* stream) {
+int canvas_bn_backward(int64_t N, int64_t C, int64_t HW, const float* x, const float* y, const uint8_t* relu_mask,
+                       const float* dy, const float* gamma, const float* save_mean, const float* save_invstd,
+                       float* dx, float* dresidual, float* dgamma, float* dbeta, int relu, void* workspace,
+                       void* stream) {
   if (N < 1 || C < 1 || HW < 1 || !x || !dy || !gamma || !save_mean || !save_invstd || !dx || !dgamma || !dbeta ||
-      !workspace || (relu && !y) || N * C * HW >= (1LL << 40)) {
+      !workspace || (relu && !y && !relu_mask) || N * C * HW >= (1LL << 40)) {
     snprintf(g_err, sizeof g_err, "canvas_bn_backward: bad arguments");
     return CANVAS_POST_ERR_ARGS;
   }
   Geo g = make_geo((int)N, (int)C, (int)HW, slices((int)N, (int)C));
   if (!aligned16(x) || !aligned16(y) || !aligned16(dy) || !aligned16(dx) || !aligned16(dresidual)) g.V = 1, g.U = g.HW;
   cudaStream_t s = (cudaStream_t)stream;
-  BwdArgs a{x, y, dy, gamma, save_mean, save_invstd, dx, dresidual, dgamma, dbeta, (double2*)workspace, relu};
+  BwdArgs a{x, y, dy, gamma, save_mean, save_invstd, dx, dresidual, dgamma, dbeta, (double2*)workspace, relu, relu_mask};
   const dim3 grid(g.P, g.C);
   if (g.V == 4) {
     bn_bwd_reduce<4><<<grid, kBlock, 0, s>>>(g, a);

@@ -26,7 +26,7 @@ import torch.nn.functional as F
 from torch import nn
 
 LIB_PATH = Path(__file__).resolve().parent / "libcanvas_post.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 _lib = None
 _lock = threading.Lock()
 
@@ -49,8 +49,8 @@ def load_library() -> ctypes.CDLL:
         lib.canvas_bn_workspace.restype = c.c_size_t
         lib.canvas_bn_workspace.argtypes = [c.c_int64] * 3
         p = c.c_void_p
-        lib.canvas_bn_forward.argtypes = [c.c_int64] * 3 + [p] * 9 + [c.c_float, c.c_float, c.c_int, p, p]
-        lib.canvas_bn_backward.argtypes = [c.c_int64] * 3 + [p] * 10 + [c.c_int, p, p]
+        lib.canvas_bn_forward.argtypes = [c.c_int64] * 3 + [p] * 9 + [c.c_float, c.c_float, c.c_int, p, p, p]
+        lib.canvas_bn_backward.argtypes = [c.c_int64] * 3 + [p] * 11 + [c.c_int, p, p]
         lib.canvas_maxpool2d_forward.argtypes = [c.c_int64] * 4 + [c.c_int] * 3 + [p] * 4
         lib.canvas_maxpool2d_backward.argtypes = [c.c_int64] * 4 + [c.c_int] * 3 + [p] * 4
         if lib.canvas_post_abi_version() != ABI_VERSION:
@@ -82,18 +82,20 @@ class _BnFn(torch.autograd.Function):
         y = torch.empty_like(x)
         mean = torch.empty(c, device=x.device, dtype=torch.float32)
         invstd = torch.empty_like(mean)
+        # ReLU mask bytes (y > 0): the backward reads 1 byte instead of y's 4 per element
+        mask = torch.empty(x.shape, device=x.device, dtype=torch.uint8) if relu else None
         ws = torch.empty(lib.canvas_bn_workspace(n, c, hw), device=x.device, dtype=torch.uint8)
         st = torch.cuda.current_stream(x.device).cuda_stream
-        _check(lib.canvas_bn_forward(n, c, hw, _ptr(x), _ptr(residual), _ptr(y), _ptr(weight), _ptr(bias), _ptr(running_mean), _ptr(running_var), _ptr(mean), _ptr(invstd), float(momentum), float(eps), int(relu), _ptr(ws), st))
+        _check(lib.canvas_bn_forward(n, c, hw, _ptr(x), _ptr(residual), _ptr(y), _ptr(weight), _ptr(bias), _ptr(running_mean), _ptr(running_var), _ptr(mean), _ptr(invstd), float(momentum), float(eps), int(relu), _ptr(mask), _ptr(ws), st))
         ctx.relu = bool(relu)
         ctx.has_res = residual is not None
-        ctx.save_for_backward(x, y if relu else None, weight, mean, invstd)
+        ctx.save_for_backward(x, mask, weight, mean, invstd)
         return y
 
     @staticmethod
     def backward(ctx, dy):
         lib = load_library()
-        x, y, weight, mean, invstd = ctx.saved_tensors
+        x, mask, weight, mean, invstd = ctx.saved_tensors
         dy = dy.contiguous()
         n, c = x.shape[0], x.shape[1]
         hw = x.numel() // max(1, n * c)
@@ -103,7 +105,7 @@ class _BnFn(torch.autograd.Function):
         db = torch.empty_like(weight)
         ws = torch.empty(lib.canvas_bn_workspace(n, c, hw), device=x.device, dtype=torch.uint8)
         st = torch.cuda.current_stream(x.device).cuda_stream
-        _check(lib.canvas_bn_backward(n, c, hw, _ptr(x), _ptr(y), _ptr(dy), _ptr(weight), _ptr(mean), _ptr(invstd), _ptr(dx), _ptr(dres), _ptr(dw), _ptr(db), int(ctx.relu), _ptr(ws), st))
+        _check(lib.canvas_bn_backward(n, c, hw, _ptr(x), None, _ptr(mask), _ptr(dy), _ptr(weight), _ptr(mean), _ptr(invstd), _ptr(dx), _ptr(dres), _ptr(dw), _ptr(db), int(ctx.relu), _ptr(ws), st))
         if ctx.has_res and not ctx.relu:
             dres = dy
         return dx, dres, dw, db, None, None, None, None, None

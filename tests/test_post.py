@@ -30,7 +30,7 @@ def test_exports_every_declared_symbol():
 
 def test_bad_arguments_fail_loudly():
     lib = post.load_library()
-    rc = lib.canvas_bn_forward(0, 4, 4, *([None] * 9), 0.1, 1e-5, 1, None, None)
+    rc = lib.canvas_bn_forward(0, 4, 4, *([None] * 9), 0.1, 1e-5, 1, None, None, None)
     assert rc == -5 and "bad arguments" in lib.canvas_post_last_error().decode()
 
 
