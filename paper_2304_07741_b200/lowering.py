@@ -42,8 +42,6 @@ from .graph import VIEW_OPS, ConcreteGraph, LoweringError
 ABI_VERSION = 1
 BLOB_MAGIC = b"CNVSBLOB"
 _IDENT = re.compile(r"[A-Za-z_]\w*")
-# fuse flat backward gradient gathers that read the same gradient (Lowerer.merge_gathers)
-MERGE_GATHERS = int(os.environ.get("CANVAS_MERGE_GATHERS", "1"))
 MAX_KSLOTS = 24  # pointers per kernel argument block (csrc/kernels/canvas_kernels.cuh)
 
 # fixed global slots; weights / grads / saved / workspace follow (see Plan.slot_*)
@@ -175,7 +173,6 @@ class Launch:
     what: str = ""  # human-readable role (profiles / DESIGN tables)
     bytes_per_image: int = 0  # algorithmic HBM bytes per image (roofline)
     flops_per_image: int = 0  # useful FLOPs per image (2 per MAC)
-    pw: dict | None = None  # flat pointwise launches: functor text, PER, slots stored (gather merging)
 
 
 @dataclass
@@ -310,7 +307,6 @@ class Fn:
         # lanes and the per-lane part by all rows: one IMAD.WIDE per gathered element
         self.uniform: set = set()
         self.loaded: dict = {}  # (slot, image stride) -> TDesc of every tensor this functor reads
-        self.stored: set = set()  # slots this functor writes (Fn.store)
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -526,7 +522,6 @@ class Fn:
         return self.fvar(f"__ldg({self.addr(d, coords)})")
 
     def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
-        self.stored.add(d.slot)
         a = self.addr(d, coords)
         if beta:
             self.emit(f"if (a.beta) *({a}) += {val}; else *({a}) = {val};")
@@ -932,7 +927,6 @@ class Lowerer:
         src += ["    " + s for s in f.pre]
         src += f.lines
         src += ["  }", "};"]
-        self._last_fn = f
         return "\n".join(src) + "\n", f.local_slots
 
     @staticmethod
@@ -971,8 +965,7 @@ class Lowerer:
             launcher = f'extern "C" __global__ void __launch_bounds__({block}) {name}(const CanvasArgs a) {{ canvas::pointwise_planes<{name}_F>(a); }}\n'
             grid = (GridRule(0, chunks, 1), GridRule(Q, 0, 1, min(65535, max(1, PLANES_CTAS // chunks))), GridRule(0, 1, 1))
         k = self.add_kernel(name, functor, launcher)
-        pw = {"per": per_image, "functor": functor, "stored": frozenset(self._last_fn.stored), "loaded": frozenset(sl for sl, _ in self._last_fn.loaded)} if planes is None else None
-        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops, pw=pw))
+        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
 
     # ---- forward
     def fwd_targets(self, v: int) -> list:
@@ -1653,92 +1646,7 @@ class Lowerer:
         self.emit_gemm_wgrad(name, afn, bfn2, O, K, S, dwslot, f"wgrad {O}x{K} over {S}/img n{u}", 4 * (nu.numel + self._input_numel(nu)), flops)
 
     # -------------------------------------------------------------- assemble
-    def _writes(self, L: Launch) -> frozenset:
-        """Slots a backward launch may write: exact for pointwise functors (their
-        stores), else every slot of the launch that is writable in the backward
-        (workspace, dx, dW; forward-saved tensors, x, dy and weights are read-only)."""
-        if L.kind == "memset":
-            return frozenset({L.memset_slot})
-        if L.pw is not None:
-            return L.pw["stored"] | frozenset(s for s in L.slots if s not in L.pw["loaded"] and s not in L.pw["stored"] and self._bwd_writable(s))
-        return frozenset(s for s in L.slots if self._bwd_writable(s))
-
-    def _bwd_writable(self, s: int) -> bool:
-        p = self.p
-        return s < 0 or s == SLOT_DX or p.slot_dw(0) <= s < p.slot_dw(0) + p.n_fc
-
-    def merge_gathers(self) -> None:
-        """Fuse two flat backward gradient gathers of the same output size that
-        read the same materialised gradient into one launch (two functors per
-        thread).  E.g. seed-7 #1's `grad n7` and `grad n1` both read the 9C FC-dgrad
-        output; fused, the second read of each image's planes hits L2 instead of
-        HBM.  Legal when the later launch B reads nothing written by the earlier
-        launch A or by any launch between them, and nothing between them touches
-        what B writes (B moves up to A's position)."""
-        if not MERGE_GATHERS:
-            return
-        p = self.p
-        L_ = p.launches
-        merged_into: dict = {}
-        j = 0
-        while j < len(L_):
-            B = L_[j]
-            done = False
-            if B.kind == "kernel" and B.phase == 1 and B.pw is not None and not B.pw.get("merged"):
-                wb = self._writes(B)
-                between_w, between_s = set(), set()
-                for i in range(j - 1, -1, -1):
-                    A = L_[i]
-                    if A.phase != 1:
-                        break
-                    between_w |= self._writes(A)
-                    between_s |= set(A.slots) | ({A.memset_slot} if A.kind == "memset" else set())
-                    if set(B.slots) & between_w:
-                        break
-                    if (A.kind == "kernel" and A.pw is not None and not A.pw.get("merged") and A.pw["per"] == B.pw["per"] and A.beta == B.beta
-                            and not (wb & between_s) and (A.pw["loaded"] & B.pw["loaded"] & {s for s in range(-len(p.ws) - 1, 0)})
-                            and len(set(A.slots) | set(B.slots)) <= MAX_KSLOTS):
-                        self._merge_pair(i, j)
-                        done = True
-                        break
-                    if wb & (set(A.slots) | ({A.memset_slot} if A.kind == "memset" else set())):
-                        break
-            if not done:
-                j += 1
-        # drop the kernels that no launch uses any more; renumber
-        used = sorted({L.kernel for L in L_ if L.kind == "kernel"})
-        remap = {k: n for n, k in enumerate(used)}
-        self.kernels = [self.kernels[k] for k in used]
-        p.kernel_names = [p.kernel_names[k] for k in used]
-        for L in L_:
-            if L.kind == "kernel":
-                L.kernel = remap[L.kernel]
-        del merged_into
-
-    def _merge_pair(self, i: int, j: int) -> None:
-        p = self.p
-        A, B = p.launches[i], p.launches[j]
-        slots = list(A.slots) + [s for s in B.slots if s not in A.slots]
-        idx = {s: slots.index(s) for s in B.slots}
-        fb = re.sub(r"a\.p\[(\d+)\]", lambda m: f"a.p[{idx[B.slots[int(m.group(1))]]}]", B.pw["functor"])
-        fa = A.pw["functor"].replace(f"struct {A.name}_F {{", "struct PA {", 1)
-        fb = fb.replace(f"struct {B.name}_F {{", "struct PB {", 1)
-        name = f"{A.name}_{B.name.split('_', 1)[1]}"
-        per = A.pw["per"]
-        body = (f"struct {name}_F {{\n" + fa + fb + f"  static constexpr long long PER = {per}LL;\n"
-                "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int r) { PA::run(a, n, r); PB::run(a, n, r); }\n};\n")
-        launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {POINTWISE_VEC}>(a); }}\n'
-        self.kernels[A.kernel] = body + launcher
-        p.kernel_names[A.kernel] = name
-        A.name, A.slots = name, tuple(slots)
-        A.what = f"{A.what} + {B.what}"
-        A.bytes_per_image += B.bytes_per_image
-        A.flops_per_image += B.flops_per_image
-        A.pw = dict(A.pw, stored=A.pw["stored"] | B.pw["stored"], loaded=A.pw["loaded"] | B.pw["loaded"], merged=True)
-        del p.launches[j]
-
     def finish(self) -> None:
-        self.merge_gathers()
         p = self.p
         nsv = len(p.saved)
         fix = lambda s: p.slot_ws(-1 - s) if s < 0 else s  # noqa: E731
