@@ -413,6 +413,85 @@ __global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2(PoolGeo g, const floa
   }
 }
 
+// 3x3 / stride 2 / pad 1 forward, W % 4 == 0: two outputs per thread from one
+// aligned float4 (input cols 4b..4b+3) + one scalar (col 4b-1) per window row;
+// float2 / 2-byte stores.  Same scan order and NaN rule as maxpool_fwd.
+__global__ void __launch_bounds__(kBlock) maxpool_fwd_k3s2_x2(PoolGeo g, const float* __restrict__ x, float* __restrict__ y,
+                                                             uint8_t* __restrict__ idx) {
+  const int OW2 = g.OW >> 1;
+  const int j = blockIdx.x * kBlock + threadIdx.x;
+  if (j >= g.OH * OW2) return;
+  const int oh = j / OW2, b = j - oh * OW2;
+  const long long planes = (long long)g.N * g.C;
+#pragma unroll 2
+  for (long long pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const float* xp = x + pl * g.H * g.W;
+    float m0 = -INFINITY, m1 = -INFINITY;
+    int b0 = 0, b1 = 0;
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      const int h = oh * 2 - 1 + kh;
+      if ((unsigned)h >= (unsigned)g.H) continue;
+      const float* row = xp + h * g.W + 4 * b;
+      const float4 q = __ldg(reinterpret_cast<const float4*>(row));
+      const float v[5] = {b > 0 ? __ldg(row - 1) : 0.f, q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        if (b > 0 || kw > 0) {  // output 2b: input col 4b-1+kw
+          const float t = v[kw];
+          if (t > m0 || isnan(t)) m0 = t, b0 = kh * 3 + kw;
+        }
+        const float t = v[kw + 2];  // output 2b+1: input col 4b+1+kw (< W: W % 4 == 0)
+        if (t > m1 || isnan(t)) m1 = t, b1 = kh * 3 + kw;
+      }
+    }
+    const long long o = pl * g.OH * g.OW + (long long)oh * g.OW + 2 * b;
+    *reinterpret_cast<float2*>(y + o) = make_float2(m0, m1);
+    *reinterpret_cast<uchar2*>(idx + o) = make_uchar2((uint8_t)b0, (uint8_t)b1);
+  }
+}
+
+// 3x3 / stride 2 / pad 1 backward, W % 4 == 0: four consecutive inputs per thread
+// (cols 4a'..4a'+3 read window cols a, a+1, a+2 with a = 2a'), float4 store.  Per
+// element the window gradients are summed in the order of maxpool_bwd_k3s2.
+__global__ void __launch_bounds__(kBlock) maxpool_bwd_k3s2_x4(PoolGeo g, const float* __restrict__ dy,
+                                                             const uint8_t* __restrict__ idx, float* __restrict__ dx) {
+  const int W4 = g.W >> 2;
+  const int j = blockIdx.x * kBlock + threadIdx.x;
+  if (j >= g.H * W4) return;
+  const int h = j / W4, w0 = (j - h * W4) * 4;
+  int rows = 1, oh0, kh0, oh1 = 0, kh1 = 0;
+  if (h & 1) {
+    oh0 = h >> 1, kh0 = 2, oh1 = (h + 1) >> 1, kh1 = 0;
+    rows = oh1 < g.OH ? 2 : 1;
+  } else {
+    oh0 = h >> 1, kh0 = 1;
+  }
+  const int a = w0 >> 1;
+  const bool c2 = a + 2 < g.OW;
+  const long long planes = (long long)g.N * g.C;
+#pragma unroll 2
+  for (long long pl = blockIdx.y; pl < planes; pl += gridDim.y) {
+    const float* dyp = dy + pl * g.OH * g.OW;
+    const uint8_t* ip = idx + pl * g.OH * g.OW;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      if (r >= rows) break;
+      const int o = (r ? oh1 : oh0) * g.OW + a, k3 = (r ? kh1 : kh0) * 3;
+      const float d0 = __ldg(dyp + o), d1 = __ldg(dyp + o + 1), d2 = c2 ? __ldg(dyp + o + 2) : 0.f;
+      const int i0 = __ldg(ip + o), i1 = __ldg(ip + o + 1), i2 = c2 ? __ldg(ip + o + 2) : 255;
+      acc.x += i0 == k3 + 1 ? d0 : 0.f;
+      acc.y += i0 == k3 + 2 ? d0 : 0.f;
+      acc.y += i1 == k3 ? d1 : 0.f;
+      acc.z += i1 == k3 + 1 ? d1 : 0.f;
+      acc.w += i1 == k3 + 2 ? d1 : 0.f;
+      acc.w += i2 == k3 ? d2 : 0.f;
+    }
+    *reinterpret_cast<float4*>(dx + pl * g.H * g.W + h * g.W + w0) = acc;
+  }
+}
+
 template <int KK, int SS, int PP>
 __global__ void __launch_bounds__(kBlock) maxpool_bwd(PoolGeo g, const float* __restrict__ dy,
                                                       const uint8_t* __restrict__ idx, float* __restrict__ dx) {
@@ -534,6 +613,13 @@ int canvas_maxpool2d_forward(int64_t N, int64_t C, int64_t H, int64_t W, int K, 
     return CANVAS_POST_ERR_ARGS;
   }
   PoolGeo g{(int)N, (int)C, (int)H, (int)W, K, S, P, (int)((H + 2 * P - K) / S + 1), (int)((W + 2 * P - K) / S + 1)};
+  if (K == 3 && S == 2 && P == 1 && W % 4 == 0 && aligned16(x) && ((uintptr_t)y & 7u) == 0 && ((uintptr_t)argmax & 1u) == 0) {
+    const int bx = (g.OH * (g.OW >> 1) + kBlock - 1) / kBlock;
+    const dim3 grid(bx, (unsigned)std::min<long long>(N * C, std::max(1, 148 * 32 / bx)));
+    maxpool_fwd_k3s2_x2<<<grid, kBlock, 0, (cudaStream_t)stream>>>(g, x, y, argmax);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_maxpool2d_forward launch", e);
+  }
   const int bx = (g.OH * g.OW + kBlock - 1) / kBlock;
   const dim3 grid(bx, (unsigned)std::min<long long>(N * C, std::max(1, 148 * 32 / bx)));
   if (K == 3 && S == 2 && P == 1)
@@ -551,6 +637,13 @@ int canvas_maxpool2d_backward(int64_t N, int64_t C, int64_t H, int64_t W, int K,
     return CANVAS_POST_ERR_ARGS;
   }
   PoolGeo g{(int)N, (int)C, (int)H, (int)W, K, S, P, (int)((H + 2 * P - K) / S + 1), (int)((W + 2 * P - K) / S + 1)};
+  if (K == 3 && S == 2 && P == 1 && W % 4 == 0 && aligned16(dx)) {
+    const int bx = (int)((H * (W >> 2) + kBlock - 1) / kBlock);
+    const dim3 grid(bx, (unsigned)std::min<long long>(N * C, std::max(1, 148 * 32 / bx)));
+    maxpool_bwd_k3s2_x4<<<grid, kBlock, 0, (cudaStream_t)stream>>>(g, dy, argmax, dx);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? CANVAS_POST_OK : fail("canvas_maxpool2d_backward launch", e);
+  }
   const int bx = (int)((H * W + kBlock - 1) / kBlock);
   const dim3 grid(bx, (unsigned)std::min<long long>(N * C, std::max(1, 148 * 32 / bx)));
   if (K == 3 && S == 2 && P == 1)
