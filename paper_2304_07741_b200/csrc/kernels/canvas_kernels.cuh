@@ -393,6 +393,13 @@ __device__ __forceinline__ void wgrad_small(const CanvasArgs& a) {
   }
 }
 
+// F::TJ > 0: partials are [M][TJ] and dW is written transposed ([TJ][M]).
+template <class F>
+__device__ __forceinline__ int reduce_out_index(const int idx) {
+  if constexpr (F::TJ > 0) return (idx % F::TJ) * (F::MJ / F::TJ) + idx / F::TJ;
+  else return idx;
+}
+
 template <class F>
 __device__ __forceinline__ void reduce_partials(const CanvasArgs& a) {
   const long long T = a.n * (long long)F::S;
@@ -403,7 +410,7 @@ __device__ __forceinline__ void reduce_partials(const CanvasArgs& a) {
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < F::MJ; idx += gridDim.x * blockDim.x) {
       float s = 0.f;
       for (int z = 0; z < Z; ++z) s += P[(long long)z * F::MJ + idx];
-      out[idx] = s;
+      out[reduce_out_index<F>(idx)] = s;
     }
     return;
   }
@@ -414,7 +421,7 @@ __device__ __forceinline__ void reduce_partials(const CanvasArgs& a) {
     for (int z = lane; z < Z; z += 32) s += P[(long long)z * F::MJ + idx];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[idx] = s;
+    if (lane == 0) out[reduce_out_index<F>(idx)] = s;
   }
 }
 

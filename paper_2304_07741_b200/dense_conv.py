@@ -91,7 +91,25 @@ def lower_conv2d(c_in: int, c_out: int, k: int, stride: int, pad: int, h_in: int
         fd.computing = None
         a_d = f"__ldg({fd.ptr(p.slot_w(0))} + (k / {kk}) * {K} + m * {kk} + (k % {kk}))"
         lw.emit_gemm_nk(f"k{len(p.kernel_names)}_bwd_dgrad_conv", fd, a_d, col2im, store_dx, M=c_in, K=Kd, S=Sd, phase=1, beta=BETA_NONE, what=f"dgrad conv {c_in}x{Kd}x{Sd}", nbytes=4 * (c_out * S + c_in * Sd), flops=2 * c_in * Kd * Sd)
-    lw.emit_gemm_wgrad(f"k{len(p.kernel_names)}_bwd_wgrad_conv", dy, im2col, c_out, K, S, p.slot_dw(0), f"wgrad conv {c_out}x{K} over {S}/img", 4 * (c_in * h_in * w_in + c_out * S), flops)
+    # wgrad orientation: MMA rows (padded to 128) take one operand, the N side
+    # (padded to 16) the other.  Put the rows on whichever side pads less overall;
+    # at the stem (K = 147, C_out = 64) that moves the im2col gathers from 256
+    # produced rows to 160 (dy takes the 128 padded rows: plain loads).
+    rows = lambda j, m: -(-j // 128) * 128 + -(-m // 16) * 16  # noqa: E731
+    wname = f"k{len(p.kernel_names)}_bwd_wgrad_conv"
+    wwhat = f"wgrad conv {c_out}x{K} over {S}/img"
+    if rows(c_out, K) < rows(K, c_out):
+
+        def im2col_m(f: Fn) -> str:  # the im2col operand indexed by the A-row variable m
+            f.emit("const int k = m;")
+            return im2col(f)
+
+        def dy_k(f: Fn) -> str:
+            return f.fvar(f"__ldg({f.ptr(SLOT_DY)} + (long long)n * {c_out * S} + k * {S} + s)")
+
+        lw.emit_gemm_wgrad(wname, im2col_m, dy_k, K, c_out, S, p.slot_dw(0), wwhat + " (transposed)", 4 * (c_in * h_in * w_in + c_out * S), flops, trans=True)
+    else:
+        lw.emit_gemm_wgrad(wname, dy, im2col, c_out, K, S, p.slot_dw(0), wwhat, 4 * (c_in * h_in * w_in + c_out * S), flops)
     lw.finish()
     return p
 

@@ -1394,8 +1394,10 @@ class Lowerer:
         self.p.launches.append(Launch("kernel", phase, name, k, 256, grid, tuple(fa.local_slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
         return False
 
-    def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops) -> None:
-        """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce."""
+    def emit_gemm_wgrad(self, name, afn, bfn, M, J, S, dw_slot, what, nbytes, flops, trans: bool = False) -> None:
+        """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce.
+        ``trans``: the reduce writes dW transposed ([J][M]) — callers swap the operand
+        roles so the costlier computed operand sits on the less padded MMA side."""
         small = M <= 16
         use_tc = self.use_tc and J >= 32 and not small
         if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
@@ -1461,7 +1463,7 @@ class Lowerer:
         # ordered reduction of the partials into dW
         rname = name + "_reduce"
         rsrc = (
-            f"struct {rname}_F {{ static constexpr int MJ = {M * J}, S = {S}, TCHUNK = {tchunk}; }};\n"
+            f"struct {rname}_F {{ static constexpr int MJ = {M * J}, S = {S}, TCHUNK = {tchunk}, TJ = {J if trans else 0}; }};\n"
             f'extern "C" __global__ void __launch_bounds__(256) {rname}(const CanvasArgs a) {{ canvas::reduce_partials<{rname}_F>(a); }}\n'
         )
         k2 = self.add_kernel(rname, "", rsrc)

@@ -119,7 +119,7 @@ void reduce_partials(const CanvasArgs& a) {
   for (int idx = 0; idx < F::MJ; ++idx) {
     float s = 0.f;
     for (int z = 0; z < Z; ++z) s += a.p[0][(long long)z * F::MJ + idx];
-    a.p[1][idx] = s;
+    a.p[1][F::TJ > 0 ? (idx % F::TJ) * (F::MJ / F::TJ) + idx / F::TJ : idx] = s;
   }
 }
 template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = 8, int NACC = 1>

@@ -71,3 +71,34 @@ def test_conv_with_input_grad_parity(cin, cout, k, stride, pad, hw):
     torch.testing.assert_close(xg.grad.cpu().double(), xr.grad, rtol=RTOL, atol=ATOL)
     err = (t.weight.grad.cpu().double() - wr.grad).abs().max() / (ATOL + RTOL * wr.grad.abs().max())
     assert err <= 1.0, float(err)
+
+
+@pytest.mark.parametrize("cin,cout,k,stride,pad,h,w", [(3, 64, 7, 2, 3, 10, 9), (16, 32, 1, 2, 0, 9, 9), (8, 16, 3, 2, 1, 13, 11)])
+def test_conv_plan_on_host_emulator(cin, cout, k, stride, pad, h, w):
+    """The generated functors (forward, dgrad gather, wgrad in both operand
+    orientations + the ordered / transposed partial reduce) run on the host
+    emulator against fp64 F.conv2d."""
+    import numpy as np
+
+    from emu.runner import EmuPlan
+
+    p = dense_conv.lower_conv2d(cin, cout, k, stride, pad, h, w, True)
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(2, cin, h, w, generator=g)
+    wt = torch.randn(cout, cin, k, k, generator=g) / (cin * k * k) ** 0.5
+    xr = x.double().requires_grad_(True)
+    wr = wt.double().requires_grad_(True)
+    yr = F.conv2d(xr, wr, stride=stride, padding=pad)
+    dy = torch.randn(yr.shape, generator=g)
+    yr.backward(dy.double())
+    em = EmuPlan(p)
+    xn, wn = x.numpy().copy(), [wt.reshape(cout, -1).numpy().copy()]
+    y = np.zeros(tuple(yr.shape), np.float32)
+    saved = [em._alloc(p.saved, 2)]
+    em.run(0, xn, wn, y=y, saved=saved)
+    dx = np.zeros_like(xn)
+    dws = [np.full_like(wn[0], np.nan)]
+    em.run(1, xn, wn, dy=dy.numpy().copy(), dx=dx, dws=dws, saved=saved)
+    torch.testing.assert_close(torch.from_numpy(y).double(), yr.detach(), rtol=RTOL, atol=ATOL)
+    torch.testing.assert_close(torch.from_numpy(dx).double(), xr.grad, rtol=RTOL, atol=ATOL)
+    torch.testing.assert_close(torch.from_numpy(dws[0]).double().view_as(wr), wr.grad, rtol=RTOL, atol=ATOL)
