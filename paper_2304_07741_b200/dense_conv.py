@@ -67,7 +67,35 @@ def lower_conv2d(c_in: int, c_out: int, k: int, stride: int, pad: int, h_in: int
     def dy(f: Fn) -> str:
         return f.fvar(f"__ldg({f.ptr(SLOT_DY)} + (long long)n * {c_out * S} + m * {S} + s)")
 
-    if dgrad:
+    if dgrad and k == 1 and pad == 0 and stride > 1:
+        # strided 1x1 (ResNet downsample): only the (stride-aligned) sampled inputs
+        # get gradient — dx[n, c, oh*S, ow*S] = sum_m W[m, c] dy[n, m, oh, ow].  The GEMM
+        # runs over the H_o*W_o sampled pixels only and its epilogue also writes the
+        # zeros of the S*S - 1 skipped positions (no memset, no zero MMA work).
+        from .lowering import SLOT_DX
+
+        def dy_plain(f: Fn) -> str:
+            return f.fvar(f"__ldg({f.ptr(SLOT_DY)} + (long long)n * {c_out * S} + k * {S} + s)")
+
+        def store_dx_strided(f: Fn, val: str) -> None:
+            f.emit(f"const int oh_ = s / {wo}; const int ow_ = s - oh_ * {wo};")
+            f.emit(f"float* const d_ = {f.ptr(SLOT_DX)} + (long long)n * {c_in * h_in * w_in} + m * {h_in * w_in} + oh_ * {stride * w_in} + ow_ * {stride};")
+            for dh in range(stride):
+                for dw in range(stride):
+                    conds = []
+                    if (ho - 1) * stride + dh >= h_in:
+                        conds.append(f"oh_ * {stride} + {dh} < {h_in}")
+                    if (wo - 1) * stride + dw >= w_in:
+                        conds.append(f"ow_ * {stride} + {dw} < {w_in}")
+                    st = f"d_[{dh * w_in + dw}] = {val if dh == 0 and dw == 0 else '0.f'};"
+                    f.emit(f"if ({' && '.join(conds)}) {st}" if conds else st)
+
+        fd = Fn(lw)
+        fd.pre = []
+        fd.computing = None
+        a_d = f"__ldg({fd.ptr(p.slot_w(0))} + k * {K} + m)"
+        lw.emit_gemm_nk(f"k{len(p.kernel_names)}_bwd_dgrad_conv", fd, a_d, dy_plain, store_dx_strided, M=c_in, K=c_out, S=S, phase=1, beta=BETA_NONE, what=f"dgrad conv 1x1/{stride} {c_in}x{c_out}x{S}", nbytes=4 * (c_out * S + c_in * h_in * w_in), flops=2 * c_in * c_out * S)
+    elif dgrad:
         # dx[n, c, ih, iw] = sum_{m, kh, kw} W[m, c, kh, kw] dy[n, m, (ih+P-kh)/S, (iw+P-kw)/S]
         Kd, Sd = c_out * kk, h_in * w_in
 

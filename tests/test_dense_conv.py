@@ -73,7 +73,7 @@ def test_conv_with_input_grad_parity(cin, cout, k, stride, pad, hw):
     assert err <= 1.0, float(err)
 
 
-@pytest.mark.parametrize("cin,cout,k,stride,pad,h,w", [(3, 64, 7, 2, 3, 10, 9), (16, 32, 1, 2, 0, 9, 9), (8, 16, 3, 2, 1, 13, 11)])
+@pytest.mark.parametrize("cin,cout,k,stride,pad,h,w", [(3, 64, 7, 2, 3, 10, 9), (16, 32, 1, 2, 0, 9, 9), (16, 32, 1, 2, 0, 10, 8), (8, 16, 1, 3, 0, 7, 8), (8, 16, 3, 2, 1, 13, 11)])
 def test_conv_plan_on_host_emulator(cin, cout, k, stride, pad, h, w):
     """The generated functors (forward, dgrad gather, wgrad in both operand
     orientations + the ordered / transposed partial reduce) run on the host
@@ -96,7 +96,7 @@ def test_conv_plan_on_host_emulator(cin, cout, k, stride, pad, h, w):
     y = np.zeros(tuple(yr.shape), np.float32)
     saved = [em._alloc(p.saved, 2)]
     em.run(0, xn, wn, y=y, saved=saved)
-    dx = np.zeros_like(xn)
+    dx = np.full_like(xn, np.nan)  # every dx element must be written (no memset in the plan)
     dws = [np.full_like(wn[0], np.nan)]
     em.run(1, xn, wn, dy=dy.numpy().copy(), dx=dx, dws=dws, saved=saved)
     torch.testing.assert_close(torch.from_numpy(y).double(), yr.detach(), rtol=RTOL, atol=ATOL)
