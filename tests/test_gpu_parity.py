@@ -131,3 +131,20 @@ def test_larger_sampled_kernels(golden, count):
         except AssertionError as e:
             bad.append(str(e)[:200])
     assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col"])
+def test_wgrad_row_groups(name, monkeypatch):
+    """The JG = 2 wgrad variant (two 128-row tiles per CTA sharing the gathered
+    output-channel operand; off by default) at a stage-2 width."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "TC_WGRAD_JG_MAX", 2)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.ALL[name], 128, 128, 28, 28, n=2)
+        assert ", 16, 2>(a)" in case.plan.source  # tc_gemm_wgrad<F, NT, STAGES, PW, JG = 2>
+        y, dx, dws = run_gpu(case)
+        assert_close(case, y, dx, dws, f"{name} JG=2")
+    finally:
+        executor._plan_cached.cache_clear()
