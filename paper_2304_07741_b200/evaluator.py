@@ -17,10 +17,17 @@ reported ``nonfinite`` (SPEC.md:506).
 
 ``evaluate_fn`` is injectable, so the dispatch logic is tested on CPU with
 fake workers (tests/test_evaluator.py).
+
+Compile-ahead (``prefetch`` > 0): plan creation is host work (lowering + NVRTC,
+~0.6 s per kernel) while timing is device work, so a worker compiles the next
+``prefetch`` kernels on host threads (the C ABI call releases the GIL) while it
+times the current one — device timings stay serial and unperturbed.  Used when
+``evaluate_fn`` carries a ``prepare`` attribute (``evaluate_kernel`` does).
 """
 
 from __future__ import annotations
 
+import collections
 import multiprocessing as mp
 import queue
 import time
@@ -53,17 +60,25 @@ class EvalResult:
 CONFIG1 = {"c_in": 64, "c_out": 64, "h": 56, "w": 56, "k": 3, "g": 4, "batch": 8}
 
 
-def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5) -> dict:
-    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events)."""
-    import torch
-
+def prepare_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5) -> dict:
+    """Host half of an evaluation: lower + compile + load (thread-safe)."""
     from .executor import device_plan, plan_for
 
+    del iters
     sh = dict(CONFIG1, **(shapes or {}))
     t0 = time.perf_counter()
     plan = plan_for(ir_text, c_in=sh["c_in"], c_out=sh["c_out"], h=sh["h"], w=sh["w"], k=sh["k"], g=sh["g"])
     dp = device_plan(plan, device)
-    plan_ms = (time.perf_counter() - t0) * 1e3
+    return {"plan": plan, "dp": dp, "plan_ms": (time.perf_counter() - t0) * 1e3}
+
+
+def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5, prepared: dict | None = None) -> dict:
+    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events)."""
+    import torch
+
+    sh = dict(CONFIG1, **(shapes or {}))
+    prepared = prepared or prepare_kernel(ir_text, device, shapes=shapes)
+    plan, dp, plan_ms = prepared["plan"], prepared["dp"], prepared["plan_ms"]
     dev = torch.device("cuda", device)
     torch.cuda.set_device(dev)
     n = sh["batch"]
@@ -102,11 +117,38 @@ def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, it
     }
 
 
-def _worker(wid: int, device: int, tasks, results, evaluate_fn, kwargs) -> None:
+evaluate_kernel.prepare = prepare_kernel
+
+
+def _hold(held, tid: int) -> None:
+    """Record a task this worker holds in shared memory (a synchronous write, so it
+    survives the worker dying with queued messages still unflushed).  Only the
+    dispatcher releases a slot, once the task's result has actually arrived."""
+    while True:
+        for i in range(len(held)):
+            if held[i] < 0:
+                held[i] = tid
+                return
+        time.sleep(0.01)  # all slots await results still in flight
+
+
+def _release(held, tid: int) -> None:
+    for i in range(len(held)):
+        if held[i] == tid:
+            held[i] = -1
+            return
+
+
+def _worker(wid: int, device: int, tasks, results, evaluate_fn, kwargs, prefetch: int = 0, held=None) -> None:
+    held = held if held is not None else [-1]
+    prep = getattr(evaluate_fn, "prepare", None) if prefetch > 0 else None
+    if prep is not None:
+        return _worker_pipelined(wid, device, tasks, results, evaluate_fn, prep, kwargs, prefetch, held)
     while True:
         t = tasks.get()
         if t is None:
             return
+        _hold(held, t.task_id)
         results.put(("start", wid, t.task_id))
         try:
             r = evaluate_fn(t.ir_text, device, **kwargs)
@@ -115,11 +157,43 @@ def _worker(wid: int, device: int, tasks, results, evaluate_fn, kwargs) -> None:
             results.put(("error", wid, EvalResult(t.task_id, "failed", worker=wid, error=f"{type(err).__name__}: {err}"[:500])))
 
 
+def _worker_pipelined(wid, device, tasks, results, evaluate_fn, prep, kwargs, prefetch, held) -> None:
+    from concurrent.futures import ThreadPoolExecutor
+
+    pool = ThreadPoolExecutor(prefetch)
+    ahead: collections.deque = collections.deque()
+    exhausted = False
+    while True:
+        while not exhausted and len(ahead) <= prefetch:
+            try:  # block only when nothing is held, so held tasks never wait on the queue
+                t = tasks.get() if not ahead else tasks.get_nowait()
+            except queue.Empty:
+                break
+            if t is None:
+                exhausted = True
+                break
+            _hold(held, t.task_id)
+            results.put(("start", wid, t.task_id))
+            ahead.append((t, pool.submit(prep, t.ir_text, device, **kwargs)))
+        if not ahead:
+            if exhausted:
+                pool.shutdown()
+                return
+            continue
+        t, fut = ahead.popleft()
+        try:
+            r = evaluate_fn(t.ir_text, device, prepared=fut.result(), **kwargs)
+            results.put(("done", wid, EvalResult(t.task_id, worker=wid, **r)))
+        except Exception as err:
+            results.put(("error", wid, EvalResult(t.task_id, "failed", worker=wid, error=f"{type(err).__name__}: {err}"[:500])))
+
+
 class CandidateEvaluator:
     """Dispatch kernels to one worker process per device; collect results in task order."""
 
-    def __init__(self, devices, evaluate_fn=evaluate_kernel, max_attempts: int = 2, **kwargs):
+    def __init__(self, devices, evaluate_fn=evaluate_kernel, max_attempts: int = 2, prefetch: int = 0, **kwargs):
         self.devices = list(devices)
+        self.prefetch = prefetch
         self.evaluate_fn = evaluate_fn
         self.max_attempts = max_attempts
         self.kwargs = kwargs
@@ -131,11 +205,13 @@ class CandidateEvaluator:
         for t in pending.values():
             tasks.put(t)
         procs = {}
+        held = {wid: ctx.Array("q", [-1] * (self.prefetch + 64), lock=False) for wid in range(len(self.devices))}
         for wid, dev in enumerate(self.devices):
-            p = ctx.Process(target=_worker, args=(wid, dev, tasks, results, self.evaluate_fn, self.kwargs), daemon=True)
+            p = ctx.Process(target=_worker, args=(wid, dev, tasks, results, self.evaluate_fn, self.kwargs, self.prefetch, held[wid]), daemon=True)
             p.start()
             procs[wid] = p
-        inflight: dict = {}  # worker -> task id
+        inflight: dict = {}  # worker -> task ids it holds
+        lost: set = set()
         done: dict[int, EvalResult] = {}
         deadline = time.monotonic() + timeout_s
         try:
@@ -145,15 +221,20 @@ class CandidateEvaluator:
                 except queue.Empty:
                     # worker lost (process died mid-task): re-queue its task
                     for wid, p in procs.items():
-                        if not p.is_alive() and wid in inflight:
-                            self._retry(pending[inflight.pop(wid)], tasks, done, "worker lost")
+                        if p.is_alive() or wid in lost:
+                            continue
+                        lost.add(wid)  # its held tasks: from shared memory (messages may be lost with it)
+                        for tid in sorted(inflight.pop(wid, set()) | {v for v in held[wid][:] if v >= 0}):
+                            if tid not in done:
+                                self._retry(pending[tid], tasks, done, "worker lost")
                     if not any(p.is_alive() for p in procs.values()):
                         break
                     continue
                 if kind == "start":
-                    inflight[wid] = payload
+                    inflight.setdefault(wid, set()).add(payload)
                     continue
-                inflight.pop(wid, None)
+                inflight.get(wid, set()).discard(payload.task_id)
+                _release(held[wid], payload.task_id)
                 if kind == "done":
                     done[payload.task_id] = payload
                 else:

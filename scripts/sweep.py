@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--out", default="")
     ap.add_argument("--nodes", type=int, default=10)
     ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--prefetch", type=int, default=-1, help="kernels compiled ahead per worker on host threads (-1: host cores per GPU - 1, max 8)")
     a = ap.parse_args()
     import torch
 
@@ -43,7 +44,8 @@ def main():
     if os.path.exists(golden):
         assert "".join(texts) == open(golden).read(), "sampler mirror diverged from the reference golden"
     t0 = time.perf_counter()
-    res = CandidateEvaluator(list(range(n))).run(texts)
+    pf = a.prefetch if a.prefetch >= 0 else min(8, max(1, (os.cpu_count() or 2) // max(n, 1) - 1))
+    res = CandidateEvaluator(list(range(n)), prefetch=pf).run(texts)
     wall = time.perf_counter() - t0
     ok = [r for r in res if r.status == "ok"]
     lat = [r.fwd_ms + r.bwd_ms for r in ok]
@@ -57,6 +59,7 @@ def main():
         "nonfinite": sum(r.status == "nonfinite" for r in res),
         "failed": sum(r.status == "failed" for r in res),
         "wall_s": round(wall, 2),
+        "compile_ahead": pf,
         "fwd_bwd_ms_median": round(statistics.median(lat), 4) if lat else None,
         "fwd_bwd_ms_p90": round(sorted(lat)[int(0.9 * (len(lat) - 1))], 4) if lat else None,
         "plan_ms_median": round(statistics.median(r.plan_ms for r in res if r.plan_ms), 1) if ok else None,

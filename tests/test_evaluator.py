@@ -45,6 +45,25 @@ def fake_die(ir, device, **kw):
     return fake_ok(ir, device)
 
 
+def fake_prepare(ir, device, **kw):
+    return {"ir": ir, "prepared_in_thread": True}
+
+
+def fake_pipelined(ir, device, prepared=None, **kw):
+    """evaluate_fn with a ``prepare`` half: the worker compiles ahead on threads."""
+    assert prepared is not None and prepared["ir"] == ir
+    if "DIE" in ir:
+        m = _mark(ir, f"pdie{kw.get('salt', '')}")
+        if not os.path.exists(m):
+            open(m, "w").close()
+            os._exit(3)
+    if "BAD" in ir:
+        raise ValueError("kernel does not lower")
+    return fake_ok(ir, device)
+
+
+fake_pipelined.prepare = fake_prepare
+
 TEXTS = [f"kernel {i}" + ("x" * i) for i in range(12)]
 
 
@@ -71,4 +90,19 @@ def test_permanent_failure_reported():
 def test_worker_death_requeues(tmp_path):
     res = CandidateEvaluator([0, 1], fake_die, salt=str(tmp_path).replace("/", "_")).run(TEXTS[:6] + ["DIE here"] + TEXTS[6:8], timeout_s=120)
     assert len(res) == 9
-    assert res[6].status == "ok"
+    # every task completes: the dead worker's held task AND results it had queued
+    # but not flushed (tracked in shared memory, released only on arrival)
+    assert all(r.status == "ok" for r in res), [(r.task_id, r.status, r.error) for r in res]
+
+
+def test_compile_ahead_pipeline():
+    """prefetch > 0: tasks held ahead by a worker are all accounted for — every
+    task exactly once, a failing one retried then failed, and every task held by a
+    worker that dies (not just the running one) re-queued."""
+    texts = TEXTS[:5] + ["BAD one"] + TEXTS[5:9] + ["DIE here"] + TEXTS[9:]
+    salt = str(os.getpid())
+    res = CandidateEvaluator([0, 1], fake_pipelined, prefetch=3, salt=salt).run(texts, timeout_s=120)
+    assert [r.task_id for r in res] == list(range(len(texts)))
+    st = {texts[r.task_id]: r.status for r in res}
+    assert st.pop("BAD one") == "failed"
+    assert all(v == "ok" for v in st.values()), st
