@@ -166,7 +166,8 @@ def device_plan(plan: Plan, device: int) -> DevicePlan:
     key = (id(plan), device)
     with _dev_lock:
         dp = _dev_plans.get(key)
-        if dp is None:
-            dp = DevicePlan(plan, device)
-            _dev_plans[key] = dp
+    if dp is not None:
         return dp
+    dp = DevicePlan(plan, device)  # NVRTC compile outside the lock: plans build in parallel
+    with _dev_lock:
+        return _dev_plans.setdefault(key, dp)
