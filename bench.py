@@ -61,11 +61,29 @@ def metric_of(model: str) -> str:
 
 
 def peaks() -> dict:
+    """Roofline denominators: MEASURED_PEAKS.json (driver-measured HBM copy
+    bandwidth, cuBLAS bf16) plus the tcgen05 TF32 / bf16 and FP32-FFMA peaks
+    measured on a B200 of this pool by scripts/peaks.cu (profiles/r02_peaks.json:
+    burst = best short launch, sustained = median over 4 s back to back)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
+            pk = json.load(f)
     except OSError:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+        pk = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "fallback": True}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_peaks.json")) as f:
+            pk["tcgen05"] = json.load(f)
+    except (OSError, ValueError):
+        pass
+    return pk
+
+
+def tf32_peak(pk: dict) -> tuple[float, str]:
+    """Sustained TF32 dense peak (TFLOP/s) for kernels timed inside a seconds-long step."""
+    t = pk.get("tcgen05", {})
+    if t.get("tf32_tcgen05_tflops_sustained"):
+        return float(t["tf32_tcgen05_tflops_sustained"]), "measured tcgen05 kind::tf32 dense peak, sustained (profiles/r02_peaks.json, scripts/peaks.cu)"
+    return pk.get("bf16_tflops_sustained", pk["bf16_tflops"]) / 2.0, "1/2 of MEASURED_PEAKS.json bf16_tflops_sustained (no measured TF32 figure)"
 
 
 def build_model(kernel: str, device=None, cpu_reference: bool = False, fuse_bn: bool = True, model: str = "resnet18"):
@@ -138,16 +156,6 @@ class CpuReference:
         F.cross_entropy(self.m(self.x), self.y).backward()
         self.opt.step()
 
-    def timed(self, budget_s: float) -> dict:
-        n, t0 = 0, time.perf_counter()
-        while True:
-            self.step()
-            n += 1
-            if time.perf_counter() - t0 >= budget_s:
-                break
-        dt = time.perf_counter() - t0
-        return {"value": n * self.batch / dt, "unit": "images/s", "cores": torch.get_num_threads(), "steps": n, "seconds": round(dt, 2), "sample": f"{n} fwd+bwd+SGD steps of batch {self.batch} at {self.x.shape[-1]}^2 through Canvas-{self.model} ({self.kernel}) in torch fp32 on CPU ({self.cores_desc()})"}
-
     @staticmethod
     def cores_desc() -> str:
         model = ""
@@ -159,25 +167,47 @@ class CpuReference:
         return f"{os.cpu_count()} threads, {model}"
 
 
-def cpu_sample(kernel: str, budget_s: float, batch: int = 2, model: str = "resnet18") -> dict:
+def cpu_full_batch(kernel: str, batch: int, model: str = "resnet18") -> dict:
+    """One full training step at the GPU arm's per-GPU batch through the CPU
+    restatement (">= 1 full batch-256 step"), after a batch-2
+    warm-up step; the same network, kernel, loss and optimizer."""
+    warm = CpuReference(kernel, 2, model)
+    warm.step()
+    del warm
     ref = CpuReference(kernel, batch, model)
-    ref.step()  # warm-up
-    return ref.timed(budget_s)
+    t0 = time.perf_counter()
+    ref.step()
+    dt = time.perf_counter() - t0
+    return {"value": batch / dt, "unit": "images/s", "cores": torch.get_num_threads(), "seconds": round(dt, 2), "same_config": True, "sample": f"1 full fwd+bwd+SGD step of batch {batch} at {ref.x.shape[-1]}^2 through Canvas-{model} ({kernel}) in torch fp32 on CPU ({CpuReference.cores_desc()}), after a batch-2 warm-up step"}
+
+
+def traffic_key(kernel: str, model: str, mod, in_shape, batch: int) -> str:
+    return f"{kernel}|{model}|{mod.in_channels}x{mod.out_channels}@{in_shape[2]}x{in_shape[3]}/s{mod.stride}|b{batch}"
 
 
 def run_reference(args, rank: int, world: int) -> None:
-    """Reference arm: the CPU restatement of the path on the host cores (rank 0 only)."""
+    """Reference arm: the CPU restatement of the path on the host cores (rank 0
+    only), on the GPU arm's config: every timed step is one full fwd+bwd+SGD
+    step at the per-GPU batch (``--batch``, 256).  Warm-up steps run at batch 2.
+    Timed steps stop early (at least one) once ``--ref-seconds`` is spent so the
+    whole run stays within a few minutes; the line says how many ran."""
     if rank != 0:
         return
-    ref = CpuReference(args.kernel, model=args.model)
-    for _ in range(args.warmup):
+    warm = CpuReference(args.kernel, batch=2, model=args.model)
+    for _ in range(max(1, args.warmup)):
+        warm.step()
+    del warm
+    ref = CpuReference(args.kernel, batch=args.batch, model=args.model)
+    times = []
+    t_all = time.perf_counter()
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
         ref.step()
-    per_step = []
-    r = None
-    for _ in range(args.steps):
-        r = ref.timed(args.ref_seconds / max(1, args.steps))
-        per_step.append(r["value"])
-    val = statistics.mean(per_step)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all >= args.ref_seconds:
+            break
+    val = args.batch * len(times) / sum(times)
+    sample = f"{len(times)} full fwd+bwd+SGD steps of batch {args.batch} at {ref.x.shape[-1]}^2 through Canvas-{args.model} ({args.kernel}) in torch fp32 on CPU ({CpuReference.cores_desc()}); {max(1, args.warmup)} batch-2 warm-up steps"
     line = {
         "impl": "reference",
         "metric": metric_of(args.model),
@@ -185,18 +215,60 @@ def run_reference(args, rank: int, world: int) -> None:
         "unit": "images/s",
         "n_gpus": world,
         "steps": args.steps,
+        "steps_timed": len(times),
         "warmup": args.warmup,
-        "ms_per_step": round(1000.0 * ref.batch / val, 1),
+        "ms_per_step": round(1000.0 * statistics.mean(times), 1),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"Canvas-{args.model} ({args.kernel}) fwd+bwd+SGD, {ref.x.shape[-1]}^2, CPU restatement, batch {ref.batch} per timed sample", "kernel": args.kernel, "model": args.model},
-        "cpu_baseline": {"value": round(val, 3), "unit": "images/s", "cores": r["cores"], "kind": "port", "sample": r["sample"]},
+        "config": {"workload": WORKLOADS[args.model] + " (CPU restatement, oracle/torch_ref.py)", "kernel": args.kernel, "model": args.model, "global_batch": args.batch, "per_gpu_batch": args.batch},
+        "cpu_baseline": {"value": round(val, 3), "unit": "images/s", "cores": torch.get_num_threads(), "kind": "port", "sample": sample, "same_config": True},
         "e2e": {"value": round(val, 3), "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def make_step(model, params, opt, world: int, bucket_mb: float = 25.0):
+    """The training step of every arm: CE loss, backward, data-parallel gradient
+    average (N > 1: bucketed all-reduce overlapped with the backward,
+    paper_2304_07741_b200.dp.GradBuckets — the only collective),
+    SGD(momentum) update.  Returns (step, fwd_bwd_update, buckets):
+    ``fwd_bwd_update`` is the capturable part (no host sync, grads live in the
+    bucket buffer for N > 1); ``step`` also resets the gradients."""
+    from paper_2304_07741_b200.dp import GradBuckets
+
+    buckets = GradBuckets(params, world, bucket_mb) if world > 1 else None
+
+    def fwd_bwd_update(xb, yb):
+        if buckets is not None:
+            buckets.zero()
+        loss = F.cross_entropy(model(xb), yb)
+        loss.backward()
+        if buckets is not None:
+            buckets.finish()
+        opt.step()
+        return loss
+
+    def step(xb, yb):
+        if buckets is None:
+            opt.zero_grad(set_to_none=True)
+        return fwd_bwd_update(xb, yb)
+
+    return step, fwd_bwd_update, buckets
+
+
+def relaunch_distributed(n: int) -> None:
+    """``--gpus N`` without a torchrun environment: re-exec this command as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    raise SystemExit(subprocess.call(cmd))
 
 
 def main() -> None:
@@ -208,8 +280,7 @@ def main() -> None:
     ap.add_argument("--kernel", default="seed7_k1", choices=sorted(zoo.ALL))
     ap.add_argument("--model", default="resnet18", help="workload backbone (backbones.SPECS): resnet18 = config 2 (default), resnet29 / resnext29_2x64d = config 3, mobilenet_v2 / efficientnet_b0 / vgg16 = config 5")
     ap.add_argument("--impl", default="canvas", choices=["canvas", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-seconds", type=float, default=30.0)
+    ap.add_argument("--ref-seconds", type=float, default=120.0, help="reference arm: stop timing full-batch CPU steps after this many seconds (>= 1 step)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-context", action="store_true")
     ap.add_argument("--no-fuse-bn", action="store_true", help="keep the backbone's cuDNN BatchNorm2d + ReLU")
@@ -217,9 +288,13 @@ def main() -> None:
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "canvas" else args.warmup
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_distributed(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -236,32 +311,12 @@ def main() -> None:
     spec = SPECS[args.model]
     model = build_model(args.kernel, dev, fuse_bn=not args.no_fuse_bn, model=args.model)
     use_graph = not args.no_graph
-    manual_sync = world > 1 and use_graph  # graph mode: no DDP, explicit all-reduce in the step
-    if world > 1 and not use_graph:
-        from torch.nn.parallel import DistributedDataParallel as DDP
-
-        model = DDP(model, device_ids=[local], bucket_cap_mb=25, gradient_as_bucket_view=True)
     params = list(model.parameters())
     opt = torch.optim.SGD(params, lr=0.01, momentum=0.9)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn(args.batch, *spec["input"], device=dev, generator=gen)
     lab = torch.randint(0, spec["classes"], (args.batch,), device=dev, generator=gen)
-
-    def fwd_bwd_update(xb, yb):
-        loss = F.cross_entropy(model(xb), yb)
-        loss.backward()
-        if manual_sync:
-            # data-parallel gradient step without DDP's host-side reducer (which
-            # cannot be captured): one NCCL all-reduce per gradient, then the mean
-            for p in params:
-                dist.all_reduce(p.grad)
-                p.grad.div_(world)
-        opt.step()
-        return loss
-
-    def step(xb, yb):
-        opt.zero_grad(set_to_none=True)
-        return fwd_bwd_update(xb, yb)
+    step, fwd_bwd_update, buckets = make_step(model, params, opt, world)
 
     t_build = time.perf_counter()
     for _ in range(args.warmup):
@@ -331,7 +386,8 @@ def main() -> None:
             for i, evs in per_rec_events.items():  # re-arm: slots 0.. are the captured launches
                 dp.profile(i, evs)
             graph = torch.cuda.CUDAGraph()
-            opt.zero_grad(set_to_none=True)
+            if buckets is None:
+                opt.zero_grad(set_to_none=True)
             with torch.cuda.graph(graph):
                 static_loss = fwd_bwd_update(static_x, static_y)
             graph.replay()
@@ -432,14 +488,14 @@ def main() -> None:
 
     # --- roofline of the dominant kernel (largest total time among the layer1 GEMMs) ---
     pk = peaks()
-    tf32_peak = pk["bf16_tflops"] / 2.0
+    tf32_pk, tf32_src = tf32_peak(pk)
     kern = []
     for i, ts in k_times.items():
         L = dp.plan.launches[i]
         avg_ms = statistics.mean(ts) if ts else float("nan")
         flops = float(L.flops_per_image) * args.batch
         ach = flops / (avg_ms * 1e-3) / 1e12
-        kern.append({"kernel": L.name, "what": L.what, "launch_ms": round(avg_ms, 4), "launches_timed": len(ts), "useful_tflops": round(ach, 2), "frac_tf32": round(ach / tf32_peak, 4), "issued_frac_tf32": round(3 * ach / tf32_peak, 4), "total_ms": sum(ts)})
+        kern.append({"kernel": L.name, "what": L.what, "launch_ms": round(avg_ms, 4), "launches_timed": len(ts), "useful_tflops": round(ach, 2), "frac_tf32": round(ach / tf32_pk, 4), "issued_frac_tf32": round(3 * ach / tf32_pk, 4), "total_ms": sum(ts)})
     if not kern:
         raise SystemExit(f"no tensor-core launch in the dominant target of {args.model}: nothing to put on the roofline")
     dom = max(kern, key=lambda r: r["total_ms"])
@@ -448,7 +504,7 @@ def main() -> None:
         "bound": "tensor",
         "kernel": dom["kernel"],
         "achieved": dom["useful_tflops"],
-        "peak": round(tf32_peak, 1),
+        "peak": round(tf32_pk, 1),
         "unit": "TFLOP/s",
         "frac": dom["frac_tf32"],
         "traffic": None,
@@ -456,16 +512,21 @@ def main() -> None:
         "launches_timed": dom["launches_timed"],
         "issued_frac": dom["issued_frac_tf32"],
         "algorithmic": f"{L.flops_per_image}*{args.batch} FLOP per launch = 2 x FC MACs of '{L.what}' (SURVEY §8d); 3xTF32 issues 3x that",
-        "peak_source": "TF32 dense = 1/2 of MEASURED_PEAKS.json bf16_tflops (burst)",
+        "peak_source": tf32_src,
         "layer1_gemms": [{k: v for k, v in r.items() if k != "total_ms"} for r in kern],
     }
+    # ncu counters of the dominant kernel, keyed by the workload that produced them:
+    # (kernel, model, dominant target c_in x c_out @ h x w / stride, batch)
+    tkey = traffic_key(args.kernel, args.model, l1, shapes[id(l1)], args.batch)
+    roofline["traffic_key"] = tkey
     prof_json = os.path.join(ROOT, "profiles", "dominant_traffic.json")
     if os.path.exists(prof_json):
         try:
             with open(prof_json) as f:
-                tr = json.load(f).get(args.kernel, {}).get(roofline["kernel"].split("_", 1)[1])
-            if tr and tr.get("batch") == args.batch:
+                tr = json.load(f).get(tkey, {}).get(roofline["kernel"].split("_", 1)[1])
+            if tr:
                 roofline["traffic"] = tr["dram_bytes"]
+                roofline["traffic_source"] = tr.get("source")
                 if tr.get("warp_instructions") and clk.get("sm_mhz"):
                     # the computed-operand GEMMs are bound by SIMT operand production,
                     # so the SM issue rate (4 warp-instructions / clock / SM) is the
@@ -475,6 +536,7 @@ def main() -> None:
                     roofline["issue"] = {"achieved_warp_inst_per_s": round(ips / 1e9, 1), "peak_warp_inst_per_s": round(148 * 4 * clk["sm_mhz"] * 1e6 / 1e9, 1), "unit": "G warp-instructions/s", "frac": round(ips / (148 * 4 * clk["sm_mhz"] * 1e6), 3), "source": tr.get("source")}
         except (OSError, ValueError):
             pass
+    net = network_roofline(core, x[:1], args.batch, ms, pk["hbm_gbs"], tf32_pk)
 
     line = {
         "metric": metric_of(args.model),
@@ -501,22 +563,103 @@ def main() -> None:
             "K": 3,
             "l2": "inputs larger than L2 (no flush)",
             "cuda_graph": graph_note,
+            "precision": "fp32 storage; FC contractions 3xTF32 on tcgen05 (hi*hi + hi*lo + lo*hi, fp32 accumulate in TMEM), everything else fp32",
+            "semantics": {"stride_policy": "x[..., ::s, ::s] first, kernel at output resolution (App. A.10)", "replication": "Fig.-2 r copies: concat (C_out = r C_in) / chunk-sum (C_in = r C_out)", "bn_post_pass": "off (SPEC.md:658); the backbone BN after each replaced conv runs as the fused native post-pass", "ties": "fold max: even split; bcast min/max: 1/2-1/2; relu'(0) = abs'(0) = 0 (App. A.5/A.6/A.8)", "bcast_order": "tile (lhs index r mod L)"},
         },
         "e2e": {"value": round(e2e, 2), "unit": "images/s", "h2d_bytes_per_step": int(xh.numel() * 4 + lh.numel() * 8), "d2h_bytes_per_step": 4},
         "gpu_launches": per_step_launches * args.steps,
         "roofline": roofline,
+        "network_roofline": net,
         "clocks": clk,
         "warmup_s": round(t_build, 1),
     }
     if rank == 0 and world == 1 and not args.no_context:
         line["context"] = context_numbers(args, dev)
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = {k: v for k, v in cpu_sample(args.kernel, args.cpu_seconds, model=args.model).items() if k in ("value", "unit", "cores", "sample")}
+        cb = cpu_full_batch(args.kernel, args.batch, model=args.model)
+        line["cpu_baseline"] = {k: v for k, v in cb.items() if k in ("value", "unit", "cores", "sample", "same_config")}
         line["cpu_baseline"]["kind"] = "port"
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def network_roofline(core, x1, batch: int, ms_step: float, hbm_gbs: float, tf32_tflops: float) -> dict:
+    """SURVEY §8(d) network roofline: roofline images/s = 1 / sum_k max(bytes_k /
+    BW, flops_k / peak_k) over every kernel the step launches, per image.
+
+    Canvas plans and the dense tcgen05 convs carry per-launch algorithmic
+    bytes / useful FLOPs (lowering.Launch); their FLOPs are counted as issued
+    3xTF32 (3 MMAs per useful MAC — the fp32-accuracy requirement, SURVEY §7
+    decision 4) against the measured tcgen05 TF32 peak.  The fused BN
+    post-pass, max-pool, head, loss and the SGD(momentum) update are
+    HBM-bound: their compulsory bytes per launch (activation reads / writes,
+    1-byte masks, 20 B per parameter for the update).  ``frac`` = measured
+    images/s / roofline images/s."""
+    from paper_2304_07741_b200.dense_conv import TcConv2d, lower_conv2d
+    from paper_2304_07741_b200.module import CanvasConv2d
+    from paper_2304_07741_b200.post import FusedBatchNorm2d, FusedMaxPool2d
+
+    io = {}
+
+    def hook(mod, i, o):
+        io[id(mod)] = (tuple(i[0].shape), tuple(o.shape), len(i) > 1 and i[1] is not None)
+
+    hooks = [m.register_forward_hook(hook) for m in core.modules() if isinstance(m, (CanvasConv2d, TcConv2d, FusedBatchNorm2d, FusedMaxPool2d, torch.nn.Linear))]
+    with torch.no_grad():
+        core(x1)
+    for h in hooks:
+        h.remove()
+    bw = hbm_gbs * 1e9
+    pk = tf32_tflops * 1e12
+    parts = {"canvas": 0.0, "dense_conv": 0.0, "bn": 0.0, "pool": 0.0, "head": 0.0, "sgd": 0.0}
+
+    def plan_time(plan):
+        t = 0.0
+        for L in plan.launches:
+            if L.kind == "kernel":
+                t += max(L.bytes_per_image / bw, 3 * L.flops_per_image / pk)
+        return t
+
+    for m in core.modules():
+        if id(m) not in io:
+            continue
+        ishape, oshape, has_res = io[id(m)]
+        ni, no = math_prod(ishape[1:]), math_prod(oshape[1:])
+        if isinstance(m, CanvasConv2d):
+            parts["canvas"] += plan_time(m.plan(ishape[2], ishape[3]))
+        elif isinstance(m, TcConv2d):
+            parts["dense_conv"] += plan_time(lower_conv2d(m.in_channels, m.out_channels, m.kernel_size[0], m.stride[0], m.padding[0], ishape[2], ishape[3], m.in_channels != 3))
+        elif isinstance(m, FusedBatchNorm2d):
+            # fwd: stats read x; apply read x (+res) write y (+1 B relu mask)
+            # bwd: reduce read dy, x (mask); apply read dy, x (mask) write dx (+dres)
+            b = 4 * ni * (1 + 2 + has_res) + (ni if m.relu else 0)
+            b += 4 * ni * (2 + 2 + 1 + (1 if has_res and m.relu else 0)) + (2 * ni if m.relu else 0)
+            parts["bn"] += b / bw
+        elif isinstance(m, FusedMaxPool2d):
+            parts["pool"] += (4 * ni + 5 * no + (5 * no + 4 * ni)) / bw
+        elif isinstance(m, torch.nn.Linear):
+            parts["head"] += max(4 * (ni + no) * 3 / bw, 3 * 2 * m.in_features * m.out_features / 74e12)
+    nparam = sum(p.numel() for p in core.parameters())
+    parts["sgd"] = 20.0 * nparam / batch / bw  # p, g, momentum read; p, momentum written (per image share)
+    t_img = sum(parts.values())
+    roof = 1.0 / t_img
+    meas = batch * 1000.0 / ms_step
+    return {
+        "roofline_images_s": round(roof, 1),
+        "measured_images_s": round(meas, 1),
+        "frac": round(meas / roof, 4),
+        "share": {k: round(v / t_img, 4) for k, v in parts.items()},
+        "how": "sum over launched kernels of max(algorithmic bytes / HBM, issued 3xTF32 FLOPs / measured TF32 tcgen05 peak) per image (SURVEY §8d); HBM = MEASURED_PEAKS.json hbm_gbs",
+    }
+
+
+def math_prod(t) -> int:
+    r = 1
+    for v in t:
+        r *= int(v)
+    return r
 
 
 def context_numbers(args, dev) -> dict:

@@ -106,6 +106,72 @@ def _unfold(x: torch.Tensor, axis: int, insert_axis: int, k: int) -> torch.Tenso
     return torch.stack(parts, dim=insert_axis)
 
 
+class NearTies:
+    """Context manager recording where a max / min decision of the forward pass
+    (bcast min/max, fold max) compares two values that differ by a nonzero
+    amount below ``rel`` of their magnitude.
+
+    Such a pair is a *branch the oracle cannot pin*: the fp64 oracle and an
+    fp32 device (different rounding of the compared values — measured up to
+    ~7e-6 relative after an FC's cancellation) may order it differently, and
+    the backward then routes a whole gradient term to the other operand
+    (App. A.6/A.8).  Exact ties (structural zeros, equal integers) are not
+    near-ties: both sides see them exactly.
+
+    ``flags`` [N]: images with any near-tie.  ``pixels`` [N, H*W] (when ``hw``
+    is given): the output pixels of decisions whose operands are laid out
+    [..., H*W] (bcast with the full spatial suffix); a near-tie that cannot be
+    localised (other layouts, fold max) flags every pixel of its image.
+    Large-batch parity tests zero dy at flagged pixels so no gradient flows
+    through those decisions on either side.
+    """
+
+    active: "NearTies | None" = None
+
+    def __init__(self, rel: float = 3e-5, hw: tuple | None = None, abs_tol: float = 0.0):
+        self.rel = rel
+        self.abs_tol = abs_tol
+        self.hw = hw
+        self.flags: torch.Tensor | None = None
+        self.pixels: torch.Tensor | None = None
+
+    def __enter__(self):
+        NearTies.active = self
+        return self
+
+    def __exit__(self, *exc):
+        NearTies.active = None
+
+    def _add(self, nb: int, img: torch.Tensor, pix: torch.Tensor | None) -> None:
+        self.flags = img if self.flags is None else self.flags | img
+        if self.hw is not None:
+            S = self.hw[0] * self.hw[1]
+            if pix is None:
+                pix = img[:, None].expand(nb, S)
+            self.pixels = pix.clone() if self.pixels is None else self.pixels | pix
+
+    def note(self, a: torch.Tensor, b: torch.Tensor) -> None:
+        with torch.no_grad():
+            d = (a - b).abs()
+            near = (d > 0) & (d <= self.rel * torch.maximum(a.abs(), b.abs()) + self.abs_tol)
+            nb = near.shape[0]
+            img = near.reshape(nb, -1).any(1)
+            pix = None
+            if self.hw is not None and near.shape[-1] == self.hw[0] * self.hw[1]:
+                pix = near.reshape(nb, -1, near.shape[-1]).any(1)
+            self._add(nb, img, pix)
+
+    def note_fold_max(self, x: torch.Tensor, dim: int) -> None:
+        if x.shape[dim] < 2:
+            return
+        with torch.no_grad():
+            top = x.topk(2, dim=dim).values
+            a, b = top.select(dim, 0), top.select(dim, 1)
+            d = (a - b).abs()
+            near = (d > 0) & (d <= self.rel * torch.maximum(a.abs(), b.abs()) + self.abs_tol)
+            self._add(near.shape[0], near.reshape(near.shape[0], -1).any(1), None)
+
+
 def run_kernel(ck: Concrete, x: torch.Tensor, weights: list[torch.Tensor]) -> torch.Tensor:
     """Forward of one kernel copy: x [N, *node0 extents] -> output node tensor."""
     vals: dict[int, torch.Tensor] = {0: x}
@@ -146,6 +212,8 @@ def run_kernel(ck: Concrete, x: torch.Tensor, weights: list[torch.Tensor]) -> to
         elif isinstance(kind, Fold):
             ax = 1 + kind.dim
             y = src.mean(dim=ax) if kind.mode == "avg" else src.amax(dim=ax)  # amax: ties split evenly (A.6)
+            if kind.mode == "max" and NearTies.active is not None:
+                NearTies.active.note_fold_max(src, ax)
         elif isinstance(kind, Softmax):
             lo, hi = 1 + kind.start, 1 + kind.end
             shp = src.shape
@@ -197,8 +265,12 @@ def _broadcast(ck: Concrete, e, lhs: torch.Tensor, rhs: torch.Tensor) -> torch.T
         o = l3 * r3
     elif op == "min":
         o = torch.minimum(l3, r3)  # ties: gradient split 1/2 - 1/2
+        if NearTies.active is not None:
+            NearTies.active.note(l3, r3)
     elif op == "max":
         o = torch.maximum(l3, r3)
+        if NearTies.active is not None:
+            NearTies.active.note(l3, r3)
     else:  # pragma: no cover
         raise ValueError(op)
     return o.reshape(rhs.shape)

@@ -25,6 +25,8 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
+#include <unistd.h>
 #include <unordered_map>
 #include <vector>
 
@@ -55,6 +57,7 @@ struct Driver {
   CUresult (*cuDevicePrimaryCtxRetain)(CUcontext*, CUdevice);
   CUresult (*cuCtxSetCurrent)(CUcontext);
   CUresult (*cuModuleLoadData)(CUmodule*, const void*);
+  CUresult (*cuModuleUnload)(CUmodule) = nullptr;
   CUresult (*cuModuleGetFunction)(CUfunction*, CUmodule, const char*);
   CUresult (*cuLaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                              CUstream, void**, void**);
@@ -82,6 +85,7 @@ struct Nvrtc {
   nvrtcResult (*cubin)(nvrtcProgram, char*);
   nvrtcResult (*destroy)(nvrtcProgram*);
   const char* (*errstr)(nvrtcResult);
+  nvrtcResult (*version)(int*, int*) = nullptr;
 };
 
 thread_local std::string g_err;
@@ -120,6 +124,7 @@ Driver& driver() {
       std::string ignore;
       sym(h, "cuEventRecordWithFlags", d.cuEventRecordWithFlags, ignore);
       sym(h, "cuStreamIsCapturing", d.cuStreamIsCapturing, ignore);
+      sym(h, "cuModuleUnload", d.cuModuleUnload, ignore);
     }
     if (d.ok && d.cuInit(0) != 0) {
       d.ok = false;
@@ -144,6 +149,8 @@ Nvrtc& nvrtc() {
            sym(h, "nvrtcGetProgramLogSize", n.logSize, w) && sym(h, "nvrtcGetProgramLog", n.log, w) &&
            sym(h, "nvrtcGetCUBINSize", n.cubinSize, w) && sym(h, "nvrtcGetCUBIN", n.cubin, w) &&
            sym(h, "nvrtcDestroyProgram", n.destroy, w) && sym(h, "nvrtcGetErrorString", n.errstr, w);
+    std::string ignore;
+    sym(h, "nvrtcVersion", n.version, ignore);
   });
   return n;
 }
@@ -192,6 +199,8 @@ struct CanvasArgs {  // must match kernels/canvas_kernels.cuh
 }  // namespace
 
 struct canvas_plan {
+  ~canvas_plan();
+  std::string module_key;  // "" until the module is acquired
   int device = 0;
   CUcontext ctx = nullptr;
   int64_t n_fc = 0, copies = 1;
@@ -221,16 +230,61 @@ void record_event(Driver& d, void* ev, CUstream st, bool external) {
     d.cuEventRecord(ev, st);
 }
 
+// Loaded modules, shared by every plan with the same (device, source):
+// reference-counted, unloaded when the last plan using one is destroyed, so a
+// long candidate search does not accumulate modules.
+struct ModEntry {
+  CUmodule mod = nullptr;
+  int64_t refs = 0;
+};
 std::mutex g_mod_mu;
-std::unordered_map<std::string, CUmodule> g_modules;  // (device, source hash) -> module
+std::unordered_map<std::string, ModEntry> g_modules;  // (device, source hash) -> module
+
+std::string module_key(const std::string& src, int device) {
+  return std::to_string(device) + ":" + std::to_string(fnv1a(src, fnv1a(kTemplates)));
+}
+
+void release_module(const std::string& key) {
+  CUmodule m = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(g_mod_mu);
+    auto it = g_modules.find(key);
+    if (it == g_modules.end() || --it->second.refs > 0) return;
+    m = it->second.mod;
+    g_modules.erase(it);
+  }
+  if (m && driver().cuModuleUnload) driver().cuModuleUnload(m);
+}
+
+// The on-disk JIT cache (CANVAS_JIT_CACHE) keys cubins by the source, the
+// templates, the target arch, the NVRTC version and the compile options, and
+// writes each through a per-process, per-thread temporary file renamed into
+// place, so concurrent evaluator workers never read a torn cubin.
+const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--extra-device-vectorization",
+                                  "-default-device"};
+constexpr int kNvrtcNOpts = 5;
+
+std::string cache_name(const std::string& src) {
+  Nvrtc& nv = nvrtc();
+  int maj = 0, mnr = 0;
+  if (nv.ok && nv.version) nv.version(&maj, &mnr);
+  uint64_t h = fnv1a(src, fnv1a(kTemplates));
+  std::string opts = "sm_100a|nvrtc" + std::to_string(maj) + "." + std::to_string(mnr);
+  for (int i = 0; i < kNvrtcNOpts; ++i) opts += std::string("|") + kNvrtcOpts[i];
+  h = fnv1a(opts, h);
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%016llx", (unsigned long long)h);
+  return std::string(buf) + ".sm_100a.cubin";
+}
 
 int compile_module(const std::string& src, int device, CUmodule* out) {
-  std::string key = std::to_string(device) + ":" + std::to_string(fnv1a(src, fnv1a(kTemplates)));
+  const std::string key = module_key(src, device);
   {
     std::lock_guard<std::mutex> lk(g_mod_mu);
     auto it = g_modules.find(key);
     if (it != g_modules.end()) {
-      *out = it->second;
+      ++it->second.refs;
+      *out = it->second.mod;
       return CANVAS_OK;
     }
   }
@@ -238,7 +292,7 @@ int compile_module(const std::string& src, int device, CUmodule* out) {
   const char* cache_dir = std::getenv("CANVAS_JIT_CACHE");
   std::string cache_path;
   if (cache_dir && *cache_dir) {
-    cache_path = std::string(cache_dir) + "/" + std::to_string(fnv1a(src, fnv1a(kTemplates))) + ".cubin";
+    cache_path = std::string(cache_dir) + "/" + cache_name(src);
     std::ifstream f(cache_path, std::ios::binary);
     if (f) cubin.assign(std::istreambuf_iterator<char>(f), std::istreambuf_iterator<char>());
   }
@@ -250,9 +304,7 @@ int compile_module(const std::string& src, int device, CUmodule* out) {
     const char* hdr_name[] = {"canvas_kernels.cuh"};
     if (nv.create(&prog, src.c_str(), "canvas_plan.cu", 1, hdr_src, hdr_name) != 0)
       return fail(CANVAS_ERR_COMPILE, "nvrtcCreateProgram failed");
-    const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--extra-device-vectorization",
-                          "-default-device"};
-    nvrtcResult rc = nv.compile(prog, 5, opts);
+    nvrtcResult rc = nv.compile(prog, kNvrtcNOpts, kNvrtcOpts);
     size_t ls = 0;
     nv.logSize(prog, &ls);
     std::string log(ls, '\0');
@@ -267,22 +319,26 @@ int compile_module(const std::string& src, int device, CUmodule* out) {
     nv.cubin(prog, &cubin[0]);
     nv.destroy(&prog);
     if (!cache_path.empty()) {
-      std::ofstream f(cache_path + ".tmp", std::ios::binary);
+      std::ostringstream tmp;
+      tmp << cache_path << ".tmp." << getpid() << "." << std::hash<std::thread::id>()(std::this_thread::get_id());
+      std::ofstream f(tmp.str(), std::ios::binary);
       f.write(cubin.data(), (std::streamsize)cubin.size());
       f.close();
-      std::rename((cache_path + ".tmp").c_str(), cache_path.c_str());
+      if (f) std::rename(tmp.str().c_str(), cache_path.c_str());
+      else std::remove(tmp.str().c_str());
     }
   }
   std::lock_guard<std::mutex> lk(g_mod_mu);
   auto it = g_modules.find(key);
   if (it != g_modules.end()) {
-    *out = it->second;
+    ++it->second.refs;
+    *out = it->second.mod;
     return CANVAS_OK;
   }
   CUmodule mod;
   CUresult r = driver().cuModuleLoadData(&mod, cubin.data());
   if (r != 0) return fail(CANVAS_ERR_CUDA, "cuModuleLoadData: " + cu_err(r));
-  g_modules[key] = mod;
+  g_modules[key] = ModEntry{mod, 1};
   *out = mod;
   return CANVAS_OK;
 }
@@ -394,6 +450,10 @@ struct Reader {
 
 }  // namespace
 
+canvas_plan::~canvas_plan() {
+  if (!module_key.empty()) release_module(module_key);
+}
+
 extern "C" {
 
 int canvas_abi_version(void) { return 1; }
@@ -476,6 +536,7 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
   CUmodule mod;
   int rc = compile_module(src, cuda_device, &mod);
   if (rc) return rc;
+  p->module_key = module_key(src, cuda_device);  // released by ~canvas_plan
   for (const auto& nm : names) {
     CUfunction f;
     e = d.cuModuleGetFunction(&f, mod, nm.c_str());
@@ -492,7 +553,7 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
   return CANVAS_OK;
 }
 
-void canvas_plan_destroy(canvas_plan* p) { delete p; }  // modules stay cached process-wide
+void canvas_plan_destroy(canvas_plan* p) { delete p; }  // unloads its module with the last plan using it
 
 int canvas_plan_query(const canvas_plan* p, int64_t batch, size_t* fwd_workspace, size_t* saved_bytes,
                       size_t* bwd_workspace) {

@@ -8,7 +8,14 @@ kernel's IR text.  A worker owns one GPU.  For each task it:
 1. solves the target shapes (config 1: N=8, C=64, H=W=56, G=4, K=3) and lowers the kernel;
 2. compiles the plan;
 3. times forward and backward on its device;
-4. optionally checks parity against the CPU oracle on a small shape.
+4. with ``parity_batch`` > 0, runs the *same* plan once more at that batch on
+   seeded CPU-drawn inputs (x ~ N(0,1) seed 0, dy ~ N(0,1) seed 1, FC weights
+   U(+-1/sqrt(fan_in)) seed 2 in IR edge order per replica — SURVEY §8d) and
+   hands the outputs to the caller's ``checker(ir_text, shapes, y, dx, dws)``,
+   which returns ``{"ok": bool, ...}``.  The checker is injected by the caller
+   (the parity tests pass one that compares against the fp64 CPU oracle); the
+   evaluator itself never imports the oracle.  A failed check is reported as
+   status ``parity_fail``.
 
 Work is partitioned as **replicas only**: there is no collective, and results return
 over host IPC.  A task whose worker fails or dies is re-queued once (SPEC.md:567
@@ -17,6 +24,13 @@ reported ``nonfinite`` (SPEC.md:506).
 
 ``evaluate_fn`` is injectable, so the dispatch logic is tested on CPU with
 fake workers (tests/test_evaluator.py).
+
+A worker whose device context is broken after a failed task (a sticky CUDA
+error such as an illegal address: every later launch in that process would
+fail too) exits; the dispatcher treats it as lost, re-queues what it held and
+starts a fresh worker process for that device (at most ``respawns`` times per
+device).  ``evaluate_fn.healthy(device)`` is the check (evaluate_kernel: a
+device synchronize).
 
 Compile-ahead (``prefetch`` > 0): plan creation is host work (lowering + NVRTC,
 ~0.6 s per kernel) while timing is device work, so a worker compiles the next
@@ -57,23 +71,67 @@ class EvalResult:
         return asdict(self)
 
 
-CONFIG1 = {"c_in": 64, "c_out": 64, "h": 56, "w": 56, "k": 3, "g": 4, "batch": 8}
+CONFIG1 = {"c_in": 64, "c_out": 64, "h": 56, "w": 56, "k": 3, "g": 4, "batch": 8, "stride": 1}
 
 
-def prepare_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5) -> dict:
+def parity_inputs(plan, shapes: dict, batch: int):
+    """Seeded CPU inputs of the parity sample (x, flat FC weights, dy) — the
+    recipe of SURVEY §8d, drawn on the host so a checker re-drawing them with
+    the same seeds sees identical bits."""
+    import math
+
+    import torch
+
+    sh = dict(CONFIG1, **shapes)
+    x = torch.randn(batch, sh["c_in"], sh["h"], sh["w"], generator=torch.Generator().manual_seed(0), dtype=torch.float32)
+    g = torch.Generator().manual_seed(2)
+    ws = []
+    for _ in range(plan.copies):
+        for v in plan.graph.fc_nodes:
+            o, k = plan.graph.fc_shape(v)
+            b = 1.0 / math.sqrt(k)
+            ws.append((torch.rand((o, k), generator=g, dtype=torch.float64) * 2 - 1).mul_(b).to(torch.float32))
+    ho, wo = -(-sh["h"] // sh["stride"]), -(-sh["w"] // sh["stride"])
+    dy = torch.randn(batch, sh["c_out"], ho, wo, generator=torch.Generator().manual_seed(1), dtype=torch.float32)
+    return x, ws, dy
+
+
+def prepare_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5, **_) -> dict:
     """Host half of an evaluation: lower + compile + load (thread-safe)."""
     from .executor import device_plan, plan_for
 
     del iters
     sh = dict(CONFIG1, **(shapes or {}))
     t0 = time.perf_counter()
-    plan = plan_for(ir_text, c_in=sh["c_in"], c_out=sh["c_out"], h=sh["h"], w=sh["w"], k=sh["k"], g=sh["g"])
+    plan = plan_for(ir_text, c_in=sh["c_in"], c_out=sh["c_out"], h=sh["h"], w=sh["w"], k=sh["k"], g=sh["g"], stride=sh["stride"])
     dp = device_plan(plan, device)
     return {"plan": plan, "dp": dp, "plan_ms": (time.perf_counter() - t0) * 1e3}
 
 
-def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5, prepared: dict | None = None) -> dict:
-    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events)."""
+def _run_once(dp, plan, x, ws, dy, device):
+    """One forward + backward of ``dp`` on device copies of host tensors -> host (y, dx, dws)."""
+    import torch
+
+    dev = torch.device("cuda", device)
+    xd, dyd = x.to(dev), dy.to(dev)
+    wd = [w.to(dev) for w in ws]
+    n = x.shape[0]
+    sb, wb = dp.sizes(n)
+    saved = torch.empty(max(sb, 1), dtype=torch.uint8, device=dev)
+    work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
+    y = torch.empty(dyd.shape, device=dev)
+    dx = torch.zeros_like(xd)
+    dws = [torch.empty_like(w) for w in wd]
+    st = torch.cuda.current_stream(dev).cuda_stream
+    dp.forward(xd, wd, y, saved, st)
+    dp.backward(xd, wd, saved, dyd, dx, dws, work, st)
+    torch.cuda.synchronize(dev)
+    return y.cpu(), dx.cpu(), [d.cpu() for d in dws]
+
+
+def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5, prepared: dict | None = None, parity_batch: int = 0, checker=None) -> dict:
+    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events);
+    with ``parity_batch`` and ``checker``: the parity sample (module doc, step 4)."""
     import torch
 
     sh = dict(CONFIG1, **(shapes or {}))
@@ -85,8 +143,8 @@ def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, it
     gen = torch.Generator(device=dev).manual_seed(0)
     x = torch.randn(n, sh["c_in"], sh["h"], sh["w"], device=dev, generator=gen)
     ws = [torch.rand(o, k_, device=dev, generator=gen).sub_(0.5).mul_(2 / k_**0.5) for _ in range(plan.copies) for o, k_ in (plan.graph.fc_shape(v) for v in plan.graph.fc_nodes)]
-    ho = -(-sh["h"] // 1)
-    y = torch.empty(n, sh["c_out"], ho, ho, device=dev)
+    ho, wo = -(-sh["h"] // sh["stride"]), -(-sh["w"] // sh["stride"])
+    y = torch.empty(n, sh["c_out"], ho, wo, device=dev)
     sb, wb = dp.sizes(n)
     saved = torch.empty(max(sb, 1), dtype=torch.uint8, device=dev)
     work = torch.empty(max(wb, 1), dtype=torch.uint8, device=dev)
@@ -107,17 +165,40 @@ def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, it
     ev[2].record()
     torch.cuda.synchronize(dev)
     finite = bool(torch.isfinite(y).all()) and bool(torch.isfinite(dx).all())
+    extra = {"launches_fwd": dp.launches(0), "launches_bwd": dp.launches(1)}
+    status = "ok" if finite else "nonfinite"
+    if parity_batch > 0 and checker is not None:
+        px, pws, pdy = parity_inputs(plan, sh, parity_batch)
+        py, pdx, pdws = _run_once(dp, plan, px, pws, pdy, device)
+        verdict = checker(ir_text, sh, py.numpy(), pdx.numpy(), [d.numpy() for d in pdws])
+        extra["parity"] = verdict
+        if status == "ok" and not verdict.get("ok", False):
+            status = "parity_fail"
     return {
-        "status": "ok" if finite else "nonfinite",
+        "status": status,
         "plan_ms": plan_ms,
         "fwd_ms": ev[0].elapsed_time(ev[1]) / iters,
         "bwd_ms": ev[1].elapsed_time(ev[2]) / iters,
         "fc_macs_per_image": plan.graph.fc_macs_per_image(),
-        "extra": {"launches_fwd": dp.launches(0), "launches_bwd": dp.launches(1)},
+        "extra": extra,
     }
 
 
+def _cuda_healthy(device: int) -> bool:
+    """False when the process's CUDA context on ``device`` is broken (sticky error)."""
+    try:
+        import torch
+
+        torch.cuda.synchronize(device)
+        torch.empty(1, device=torch.device("cuda", device)).add_(1)
+        torch.cuda.synchronize(device)
+        return True
+    except Exception:
+        return False
+
+
 evaluate_kernel.prepare = prepare_kernel
+evaluate_kernel.healthy = _cuda_healthy
 
 
 def _hold(held, tid: int) -> None:
@@ -139,6 +220,18 @@ def _release(held, tid: int) -> None:
             return
 
 
+def _exit_if_broken(evaluate_fn, device: int, results) -> None:
+    """After a failed task: a worker whose device context is broken exits (its
+    held tasks are re-queued and a fresh worker replaces it, module doc)."""
+    healthy = getattr(evaluate_fn, "healthy", None)
+    if healthy is not None and not healthy(device):
+        results.close()
+        results.join_thread()  # flush the error report before dying
+        import os
+
+        os._exit(70)
+
+
 def _worker(wid: int, device: int, tasks, results, evaluate_fn, kwargs, prefetch: int = 0, held=None) -> None:
     held = held if held is not None else [-1]
     prep = getattr(evaluate_fn, "prepare", None) if prefetch > 0 else None
@@ -155,6 +248,7 @@ def _worker(wid: int, device: int, tasks, results, evaluate_fn, kwargs, prefetch
             results.put(("done", wid, EvalResult(t.task_id, worker=wid, **r)))
         except Exception as err:  # reported, re-queued by the dispatcher
             results.put(("error", wid, EvalResult(t.task_id, "failed", worker=wid, error=f"{type(err).__name__}: {err}"[:500])))
+            _exit_if_broken(evaluate_fn, device, results)
 
 
 def _worker_pipelined(wid, device, tasks, results, evaluate_fn, prep, kwargs, prefetch, held) -> None:
@@ -186,16 +280,18 @@ def _worker_pipelined(wid, device, tasks, results, evaluate_fn, prep, kwargs, pr
             results.put(("done", wid, EvalResult(t.task_id, worker=wid, **r)))
         except Exception as err:
             results.put(("error", wid, EvalResult(t.task_id, "failed", worker=wid, error=f"{type(err).__name__}: {err}"[:500])))
+            _exit_if_broken(evaluate_fn, device, results)
 
 
 class CandidateEvaluator:
     """Dispatch kernels to one worker process per device; collect results in task order."""
 
-    def __init__(self, devices, evaluate_fn=evaluate_kernel, max_attempts: int = 2, prefetch: int = 0, **kwargs):
+    def __init__(self, devices, evaluate_fn=evaluate_kernel, max_attempts: int = 2, prefetch: int = 0, respawns: int = 3, **kwargs):
         self.devices = list(devices)
         self.prefetch = prefetch
         self.evaluate_fn = evaluate_fn
         self.max_attempts = max_attempts
+        self.respawns = respawns
         self.kwargs = kwargs
 
     def run(self, ir_texts, timeout_s: float = 3600.0) -> list[EvalResult]:
@@ -205,11 +301,19 @@ class CandidateEvaluator:
         for t in pending.values():
             tasks.put(t)
         procs = {}
-        held = {wid: ctx.Array("q", [-1] * (self.prefetch + 64), lock=False) for wid in range(len(self.devices))}
-        for wid, dev in enumerate(self.devices):
+        held = {}
+        device_of = {}
+
+        def spawn(wid: int, dev: int) -> None:
+            held[wid] = ctx.Array("q", [-1] * (self.prefetch + 64), lock=False)
+            device_of[wid] = dev
             p = ctx.Process(target=_worker, args=(wid, dev, tasks, results, self.evaluate_fn, self.kwargs, self.prefetch, held[wid]), daemon=True)
             p.start()
             procs[wid] = p
+
+        for wid, dev in enumerate(self.devices):
+            spawn(wid, dev)
+        respawned = {dev: 0 for dev in self.devices}
         inflight: dict = {}  # worker -> task ids it holds
         lost: set = set()
         done: dict[int, EvalResult] = {}
@@ -227,6 +331,11 @@ class CandidateEvaluator:
                         for tid in sorted(inflight.pop(wid, set()) | {v for v in held[wid][:] if v >= 0}):
                             if tid not in done:
                                 self._retry(pending[tid], tasks, done, "worker lost")
+                        dev = device_of[wid]
+                        if respawned[dev] < self.respawns and len(done) < len(pending):
+                            respawned[dev] += 1  # a fresh process (fresh CUDA context) for that device
+                            spawn(max(procs) + 1, dev)
+                        break  # procs changed size
                     if not any(p.is_alive() for p in procs.values()):
                         break
                     continue

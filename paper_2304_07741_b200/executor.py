@@ -14,8 +14,10 @@ construction raises.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import functools
+import hashlib
 import threading
 from pathlib import Path
 
@@ -158,16 +160,27 @@ class DevicePlan:
         )
 
 
-_dev_plans: dict = {}
+_DEV_PLAN_CACHE = 512  # compiled plans kept alive by the cache (LRU); callers may hold more
+_dev_plans: "collections.OrderedDict[tuple, DevicePlan]" = collections.OrderedDict()
 _dev_lock = threading.Lock()
 
 
 def device_plan(plan: Plan, device: int) -> DevicePlan:
-    key = (id(plan), device)
+    """The compiled plan of ``plan`` on ``device``, shared by every caller with the
+    same plan content (keyed by the blob digest, not the Python object).  The
+    cache is a bounded LRU: an evicted plan is destroyed (and its module unloaded
+    by the runtime) once no caller holds it, so long searches stay bounded."""
+    blob = plan.blob()
+    key = (hashlib.sha1(blob).hexdigest(), device)
     with _dev_lock:
         dp = _dev_plans.get(key)
-    if dp is not None:
-        return dp
+        if dp is not None:
+            _dev_plans.move_to_end(key)
+            return dp
     dp = DevicePlan(plan, device)  # NVRTC compile outside the lock: plans build in parallel
     with _dev_lock:
-        return _dev_plans.setdefault(key, dp)
+        got = _dev_plans.setdefault(key, dp)
+        _dev_plans.move_to_end(key)
+        while len(_dev_plans) > _DEV_PLAN_CACHE:
+            _dev_plans.popitem(last=False)
+        return got

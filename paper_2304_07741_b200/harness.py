@@ -55,6 +55,13 @@ def prune_threshold(rule: PruneRule, epoch: int, total_epochs: int) -> float | N
     return rule.lam(epoch / total_epochs) * rule.best_curve[epoch]
 
 
+def final_epoch_index(epochs: int) -> int:
+    """``total_epochs`` argument for curves reported at epochs 0 .. E-1: the index
+    of the final epoch, so that lambda reaches 1 there ("final epoch:
+    threshold = best[last] exactly") while epoch 0 stays at theta (SPEC.md:560)."""
+    return max(epochs - 1, 1)
+
+
 def prune_decision(rule: PruneRule, candidate: list, epoch: int, total_epochs: int) -> str:
     """'prune' iff candidate[epoch] < lambda(epoch / total) * best[epoch], else 'continue'."""
     thr = prune_threshold(rule, epoch, total_epochs)
@@ -115,7 +122,8 @@ class Leaderboard:
 def _worker(wid: int, inbox, results, train_fn, kwargs) -> None:
     """Worker loop: tasks and prune/continue answers arrive on ``inbox`` (the
     dispatcher assigns each task to one worker, so it always knows what a lost
-    worker held)."""
+    worker held).  The first message is ``ready`` (the process is up)."""
+    results.put({"type": "ready", "worker": wid, "task_id": -1})
     while True:
         t = inbox.get()
         if t is None:
@@ -143,8 +151,13 @@ class _Pruned(Exception):
 class Dispatcher:
     """Runs HarnessTasks on ``workers`` processes with accuracy-curve pruning."""
 
-    def __init__(self, workers: int, train_fn, rule: PruneRule | None = None, max_attempts: int = 2, budget=None, **kwargs):
+    def __init__(self, workers: int, train_fn, rule: PruneRule | None = None, max_attempts: int = 2, budget=None, warm_start: bool = False, **kwargs):
         self.n = workers
+        # warm_start: start every worker and wait for its ``ready`` before the first
+        # task, so process start-up is not charged to the dispatch (steady state,
+        # SPEC.md:679 simulated-worker throughput); ``timing`` records both phases
+        self.warm_start = warm_start
+        self.timing: dict = {}
         self.train_fn = train_fn
         self.board = Leaderboard(rule)
         self.max_attempts = max_attempts
@@ -181,9 +194,27 @@ class Dispatcher:
                 procs[w][1].put(t)
                 return
 
-        for _ in range(min(self.n, len(tasks))):
-            assign(spawn())
+        t_spawn = time.monotonic()
+        first = [spawn() for _ in range(min(self.n, len(tasks)))]
         deadline = time.monotonic() + timeout_s
+        early: list = []
+        if self.warm_start:
+            ready: set = set()
+            while len(ready) < len(first) and time.monotonic() < deadline:
+                try:
+                    m = rq.get(timeout=0.2)
+                except queue.Empty:
+                    if any(not procs[w][0].is_alive() for w in first):
+                        break
+                    continue
+                if m["type"] == "ready":
+                    ready.add(m["worker"])
+                else:
+                    early.append(m)
+        t_run = time.monotonic()
+        self.timing = {"startup_s": t_run - t_spawn}
+        for w in first:
+            assign(w)
         try:
             while len(self.board.entries) < len(pending) and time.monotonic() < deadline:
                 for w in [w for w in inflight if not procs[w][0].is_alive()]:  # WorkerLost
@@ -193,8 +224,10 @@ class Dispatcher:
                 if not inflight and not todo:
                     break
                 try:
-                    m = rq.get(timeout=0.2)
+                    m = early.pop() if early else rq.get(timeout=0.2)
                 except queue.Empty:
+                    continue
+                if m["type"] == "ready":
                     continue
                 w, tid = m["worker"], m["task_id"]
                 if w not in procs or inflight.get(w) != tid:
@@ -203,8 +236,9 @@ class Dispatcher:
                     c = curves[tid]
                     c.append(m["accuracy"])
                     t = pending[tid]
-                    if prune_decision(self.board.rule, c, m["epoch"], t.epochs) == "prune":
-                        thr = prune_threshold(self.board.rule, m["epoch"], t.epochs)
+                    last = final_epoch_index(t.epochs)  # epochs are reported 0 .. E-1
+                    if prune_decision(self.board.rule, c, m["epoch"], last) == "prune":
+                        thr = prune_threshold(self.board.rule, m["epoch"], last)
                         msg = {"type": "prune", "task_id": tid, "reason": f"accuracy {m['accuracy']:.4f} < {thr:.4f} at epoch {m['epoch']}"}
                         self.messages.append(msg)
                         self.board.record(Entry(tid, "pruned", list(c), c[-1], reason=msg["reason"], worker=w))
@@ -221,6 +255,7 @@ class Dispatcher:
                     self._retry(pending[tid], todo, m.get("reason", "error"))
                 assign(w)
         finally:
+            self.timing["run_s"] = time.monotonic() - t_run
             for p, inbox in procs.values():
                 inbox.put(None)
             for p, _ in procs.values():

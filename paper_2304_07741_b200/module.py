@@ -83,6 +83,13 @@ class CanvasConv2d(nn.Module):
         self.bias = nn.Parameter(torch.zeros(out_channels)) if bias else None
         self._plans: dict = {}
 
+    def __getstate__(self):
+        """Compiled device plans (ctypes handles) are a cache: dropped on
+        copy / pickle and rebuilt lazily (deduplicated by executor.device_plan)."""
+        state = self.__dict__.copy()
+        state["_plans"] = {}
+        return state
+
     def out_hw(self, h: int, w: int) -> tuple[int, int]:
         return -(-h // self.stride), -(-w // self.stride)
 

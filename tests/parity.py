@@ -71,3 +71,15 @@ def assert_close(case: Case, y, dx, dws, what: str = "") -> dict:
     bad = {k: v for k, v in r.items() if not v <= 1.0}
     assert not bad, f"{what} parity failure (ratio to tolerance > 1): {bad}"
     return r
+
+
+def oracle_checker(ir_text: str, shapes: dict, y, dx, dws) -> dict:
+    """Parity checker for CandidateEvaluator (its ``checker`` hook): re-draws the
+    evaluator's seeded inputs (same recipe: evaluator.parity_inputs / §8d),
+    runs the fp64 oracle and compares with the north-star tolerances."""
+    case = reference(ir_text, shapes["c_in"], shapes["c_out"], shapes["h"], shapes["w"], stride=shapes.get("stride", 1), n=y.shape[0], g=shapes.get("g", 4), k=shapes.get("k", 3))
+    try:
+        r = assert_close(case, y, dx, dws, "evaluator parity sample")
+        return {"ok": True, "ratios": {k: round(v, 4) for k, v in r.items()}}
+    except AssertionError as e:
+        return {"ok": False, "error": str(e)[:300]}

@@ -76,3 +76,25 @@ def test_module_refuses_cpu():
     m = CanvasConv2d(zoo.SEED7_K1, 8, 8)
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         m(torch.randn(1, 8, 6, 6))
+
+
+def test_canvas_module_copy_and_pickle_drop_plan_cache():
+    """a used CanvasConv2d holds ctypes plan handles; deepcopy / pickle
+    must drop that cache instead of failing."""
+    import copy
+    import io
+
+    import torch
+
+    from paper_2304_07741_b200 import zoo
+    from paper_2304_07741_b200.module import CanvasConv2d
+
+    m = CanvasConv2d(zoo.SEED7_K1, 16, 32, 3)
+    m._plans[(8, 8, 0)] = object()  # stands in for a DevicePlan (ctypes handle)
+    m2 = copy.deepcopy(m)
+    assert m2._plans == {} and m._plans
+    buf = io.BytesIO()
+    torch.save(m, buf)
+    buf.seek(0)
+    m3 = torch.load(buf, weights_only=False)
+    assert m3._plans == {} and all(torch.equal(a, b) for a, b in zip(m3.weights, m.weights))

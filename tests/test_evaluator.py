@@ -64,6 +64,38 @@ def fake_pipelined(ir, device, prepared=None, **kw):
 
 fake_pipelined.prepare = fake_prepare
 
+
+def fake_sticky(ir, device, **kw):
+    """A kernel that faults and leaves the process's device context broken
+    (like an illegal address): every later task in that process fails too."""
+    flag = _sticky_flag()
+    if os.path.exists(flag):
+        raise RuntimeError("CUDA error: an illegal memory access was encountered (sticky)")
+    if "FAULT" in ir:
+        open(flag, "w").close()
+        raise RuntimeError("CUDA error: an illegal memory access was encountered")
+    return fake_ok(ir, device)
+
+
+def _sticky_flag():
+    return _mark("sticky", f"proc{os.getpid()}-{os.environ.get('CANVAS_STICKY_SALT', '')}")
+
+
+fake_sticky.healthy = lambda device: not os.path.exists(_sticky_flag())
+
+
+def fake_parity(ir, device, **kw):
+    r = fake_ok(ir, device)
+    verdict = kw["checker"](ir, {}, None, None, [])
+    r["extra"]["parity"] = verdict
+    if not verdict["ok"]:
+        r["status"] = "parity_fail"
+    return r
+
+
+def check_no_odd(ir, shapes, y, dx, dws):
+    return {"ok": "odd" not in ir}
+
 TEXTS = [f"kernel {i}" + ("x" * i) for i in range(12)]
 
 
@@ -106,3 +138,29 @@ def test_compile_ahead_pipeline():
     st = {texts[r.task_id]: r.status for r in res}
     assert st.pop("BAD one") == "failed"
     assert all(v == "ok" for v in st.values()), st
+
+
+def test_single_device_survives_worker_crash(tmp_path):
+    """One device: a worker that dies is replaced by a fresh process, so the
+    sweep still completes (a dead worker used to end a 1-GPU sweep)."""
+    res = CandidateEvaluator([0], fake_die, salt=str(tmp_path).replace("/", "_")).run(TEXTS[:3] + ["DIE here"] + TEXTS[3:6], timeout_s=120)
+    assert all(r.status == "ok" for r in res), [(r.task_id, r.status, r.error) for r in res]
+
+
+def test_broken_context_worker_exits_and_is_replaced(monkeypatch):
+    """After a fault that breaks the device context, the worker exits instead of
+    failing every later task; the faulting task is retried on a fresh worker
+    (and fails again there), every other task succeeds."""
+    monkeypatch.setenv("CANVAS_STICKY_SALT", f"{os.getpid()}-{os.urandom(4).hex()}")  # inherited by the workers
+    texts = TEXTS[:3] + ["FAULT kernel"] + TEXTS[3:8]
+    res = CandidateEvaluator([0], fake_sticky, respawns=4).run(texts, timeout_s=120)
+    st = [r.status for r in res]
+    assert st[3] == "failed" and "illegal" in res[3].error
+    assert st[:3] + st[4:] == ["ok"] * 8, [(r.task_id, r.status, r.error) for r in res]
+
+
+def test_parity_checker_injected():
+    """The caller's checker decides parity; failures are reported as parity_fail."""
+    res = CandidateEvaluator([0, 1], fake_parity, checker=check_no_odd).run(["k even", "k odd", "k even2"], timeout_s=120)
+    assert [r.status for r in res] == ["ok", "parity_fail", "ok"]
+    assert res[1].extra["parity"] == {"ok": False}
