@@ -779,9 +779,10 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
         for (int q = 0; q < ROWS; ++q) {
           const int k = kb * kBK + warp * ROWS + q;
           const int kc = k < F::K ? k : F::K - 1;
+          const typename F::BR R = F::Brow(a, kc);  // row context: once per (k-block, row)
 #pragma unroll
           for (int mb = 0; mb < 4; ++mb) {
-            const float v = F::B(a, (long long)pn[mb], kc, ps[mb]);
+            const float v = F::Bk(a, R, (long long)pn[mb], ps[mb]);
             const bool ok = ((okmask >> mb) & 1u) && k < F::K;
             va[q][mb] = ok ? v : 0.f;
             // operand write-back for the wgrad (coalesced along the lane = pixel)
@@ -1009,9 +1010,10 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
         for (int q = 0; q < ROWS; ++q) {
           const int k = kb * kBK + warp * ROWS + q;
           const int kc = k < F::K ? k : F::K - 1;
+          const typename F::BR R = F::Brow(a, kc);
 #pragma unroll
           for (int mb = 0; mb < 4; ++mb) {
-            const float v = F::B(a, (long long)pn[mb], kc, ps[mb]);
+            const float v = F::Bk(a, R, (long long)pn[mb], ps[mb]);
             va[q][mb] = (((okmask >> mb) & 1u) && k < F::K) ? v : 0.f;
           }
         }
@@ -1204,6 +1206,21 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     // decomposition per k-block); warp w owns rows w, w+8, ... (channel index
     // math is warp-uniform); each warp writes whole 128 B swizzled rows.
     constexpr int RA = kBM * JG / PW, RB = (NT + PW - 1) / PW;
+    // row contexts (channel decomposition, tap and base offsets of each row the
+    // warp owns) are fixed for the CTA: built once here, so a gathered element
+    // costs only its per-pixel part (F::Ak / F::Bk)
+    typename F::BR rb[RA];
+    typename F::AR ra[RB];
+#pragma unroll
+    for (int w = 0; w < RA; ++w) {
+      const int jj = j0 + warp + PW * w;
+      rb[w] = F::Brow(a, jj < F::J ? jj : F::J - 1);
+    }
+#pragma unroll
+    for (int w = 0; w < RB; ++w) {
+      const int mm = m0 + warp + PW * w;
+      ra[w] = F::Arow(a, mm < F::M ? mm : F::M - 1);
+    }
     float va[RA], vb[RB];
     auto gather = [&](int kb) {
       const long long t = tbeg + (long long)kb * kBK + lane;
@@ -1211,18 +1228,15 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       const long long tc = ok ? t : tbeg;
       const long long n = tc / F::S;
       const int s = (int)(tc - n * F::S);
+      // rows past J / M read a clamped valid row: their accumulator rows and
+      // columns are never stored, so only pixels past the chunk end need zeros —
+      // and zeroing one operand (A, the fewer rows) zeroes their products
 #pragma unroll
-      for (int w = 0; w < RA; ++w) {
-        const int jj = j0 + warp + PW * w;
-        const float v = F::B(a, n, jj < F::J ? jj : F::J - 1, s);
-        va[w] = (ok && jj < F::J) ? v : 0.f;
-      }
+      for (int w = 0; w < RA; ++w) va[w] = F::Bk(a, rb[w], n, s);
 #pragma unroll
       for (int w = 0; w < RB; ++w) {
-        const int row = warp + PW * w;
-        const int mm = m0 + row;
-        const float v = F::A(a, n, mm < F::M ? mm : F::M - 1, s);
-        vb[w] = (ok && mm < F::M && row < NT) ? v : 0.f;
+        const float v = F::Ak(a, ra[w], n, s);
+        vb[w] = (ok && warp + PW * w < NT) ? v : 0.f;
       }
     };
     const int off_l = ((lane >> 2) << 4) | ((lane & 3) << 2);  // chunk/word of this pixel before the swizzle
@@ -1251,7 +1265,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
         const int row = warp + PW * w;  // tile row >> 7, row & 127 inside it (tiles are contiguous)
-        const int off = row * 128 + (off_l ^ ((row & 7) << 4));
+        const int off = row * 128 + (off_l ^ (((PW % 8 == 0 ? warp : row) & 7) << 4));
         float h, l;
         split_tf32(va[w], h, l);
         *reinterpret_cast<float*>(sa_hi + off) = h;
@@ -1261,7 +1275,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       for (int w = 0; w < RB; ++w) {
         const int row = warp + PW * w;
         if (row < NT) {
-          const int off = row * 128 + (off_l ^ ((row & 7) << 4));
+          const int off = row * 128 + (off_l ^ (((PW % 8 == 0 ? warp : row) & 7) << 4));
           float h, l;
           split_tf32(vb[w], h, l);
           *reinterpret_cast<float*>(sb_hi + off) = h;

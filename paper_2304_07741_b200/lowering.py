@@ -306,6 +306,12 @@ class Fn:
         # as (per-lane part) + (uniform part) so the uniform part is shared by all
         # lanes and the per-lane part by all rows: one IMAD.WIDE per gathered element
         self.uniform: set = set()
+        # hoist: uniform ivars (functions of the uniform row variable only) are
+        # emitted into ``uni_lines`` — the functor's row context, evaluated once
+        # per row by the GEMM producers instead of once per element
+        self.hoist = False
+        self.uni_lines: list[str] = []
+        self.uni_vars: list[str] = []
         self.loaded: dict = {}  # (slot, image stride) -> TDesc of every tensor this functor reads
 
     # -- bookkeeping -----------------------------------------------------------
@@ -348,9 +354,14 @@ class Fn:
         if got:
             return got
         v = self.fresh("i")
-        self.emit(f"const int {v} = {expr};")
+        uni = bool(self.uniform) and all(t in self.uniform for t in _IDENT.findall(expr))
+        if uni and self.hoist:
+            self.uni_lines.append(f"const int {v} = {expr};")
+            self.uni_vars.append(v)
+        else:
+            self.emit(f"const int {v} = {expr};")
         self.memo_put(("i", expr), v)
-        if self.uniform and all(t in self.uniform for t in _IDENT.findall(expr)):
+        if uni:
             self.uniform.add(v)
         return v
 
@@ -1268,6 +1279,30 @@ class Lowerer:
                 self.p.saved[sidx] = SizeRule(0, 1, 0)  # path without operand write-back: no buffer
 
     @staticmethod
+    def split_operand(name: str, f: Fn, val: str, uvar: str) -> list:
+        """Operand functor in row-split form: ``{name}R`` holds the row context
+        (every index term that depends on the row variable ``uvar`` only — channel
+        decompositions, tap offsets, per-row base offsets), ``{name}row(a, uvar)``
+        computes it, ``{name}k(a, R, n, s)`` evaluates one element from it.  The
+        tcgen05 producers whose rows are fixed for a whole CTA (wgrad) build the
+        row contexts once and pay only the per-pixel part per element;
+        ``{name}(a, n, uvar, s)`` composes the two for the other templates."""
+        mem = f.uni_vars
+        out = [f"  struct {name}R {{ int {', '.join(mem) if mem else '_unused'}; }};"]
+        out.append(f"  static __device__ __forceinline__ {name}R {name}row(const CanvasArgs& a, const int {uvar}) {{")
+        out += ["    " + ln for ln in f.uni_lines]
+        out.append(f"    {name}R R;")
+        out += [f"    R.{v} = {v};" for v in mem]
+        if not mem:
+            out.append("    R._unused = 0;")
+        out += ["    return R;", "  }"]
+        out.append(f"  static __device__ __forceinline__ float {name}k(const CanvasArgs& a, const {name}R& R, const long long n, const int s) {{")
+        out += [f"    const int {v} = R.{v};" for v in mem]
+        out += ["    " + ln for ln in f.pre] + f.lines + [f"    return {val};", "  }"]
+        out.append(f"  static __device__ __forceinline__ float {name}(const CanvasArgs& a, const long long n, const int {uvar}, const int s) {{ return {name}k(a, {name}row(a, {uvar}), n, s); }}")
+        return out
+
+    @staticmethod
     def prefetch_members(f: Fn, fns, S: int) -> list:
         """``NPF`` / ``pf_addr``: one 128 B line per row of every materialised
         tensor the producer functors ``fns`` read, at pixel (n, s) — the
@@ -1303,6 +1338,7 @@ class Lowerer:
         fb.computing = None
         fb.local_slots = fa.local_slots  # share the pointer table
         fb.uniform = {"k"}  # tcgen05 producers: k-row per warp, lane = pixel
+        fb.hoist = True
         bval = bfn(fb)
         fs = Fn(self)
         fs.pre = []
@@ -1316,9 +1352,8 @@ class Lowerer:
             "  static __device__ __forceinline__ float A(const CanvasArgs& a, const int m, const int k) {",
             f"    return {a_expr};",
             "  }",
-            "  static __device__ __forceinline__ float B(const CanvasArgs& a, const long long n, const int k, const int s) {",
         ]
-        lines += ["    " + s for s in fb.pre] + fb.lines + [f"    return {bval};", "  }"]
+        lines += self.split_operand("B", fb, bval, "k")
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
         tc = self.use_tc and M >= 8 and K >= 16
@@ -1417,17 +1452,16 @@ class Lowerer:
         fa.computing = fb.computing = None
         fb.local_slots = fa.local_slots
         fa.uniform, fb.uniform = {"m"}, {"k"}  # tcgen05 wgrad producers: row per warp, lane = pixel
+        fa.hoist = fb.hoist = True
         aval = afn(fa)
         bval = bfn(fb)
         pslot_local = fa.ptr(-1 - k_ws)  # partials (fixed up to the real ws slot in finish())
         lines = [
             f"struct {name}_F {{",
             f"  static constexpr int M = {M}, J = {J}, S = {S}, TCHUNK = {tchunk};",
-            "  static __device__ __forceinline__ float A(const CanvasArgs& a, const long long n, const int m, const int s) {",
         ]
-        lines += ["    " + s for s in fa.pre] + fa.lines + [f"    return {aval};", "  }"]
-        lines += ["  static __device__ __forceinline__ float B(const CanvasArgs& a, const long long n, const int k, const int s) {"]
-        lines += ["    " + s for s in fb.pre] + fb.lines + [f"    return {bval};", "  }"]
+        lines += self.split_operand("A", fa, aval, "m")
+        lines += self.split_operand("B", fb, bval, "k")
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
         lines += self.prefetch_members(fa, [fb, fa], S)
         lines += ["};"]
