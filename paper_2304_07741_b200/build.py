@@ -78,9 +78,14 @@ def pinned_source() -> str:
     from . import zoo
     from .executor import plan_for
 
+    from .dense_conv import lower_conv2d
+
+    plans = [(name, plan_for(text, c_in=64, c_out=64, h=56, w=56, k=3, g=4)) for name, text in zoo.ALL.items()]
+    # dense backbone convs (ResNet stem 7x7/2 and a strided 1x1 downsample with dgrad)
+    plans.append(("stem", lower_conv2d(3, 64, 7, 2, 3, 224, 224, False)))
+    plans.append(("down", lower_conv2d(64, 128, 1, 2, 0, 56, 56, True)))
     parts = []
-    for name, text in zoo.ALL.items():
-        p = plan_for(text, c_in=64, c_out=64, h=56, w=56, k=3, g=4)
+    for name, p in plans:
         src = p.source.replace('#include "canvas_kernels.cuh"\n', "")
         # kernel names are per-plan; prefix them so one translation unit holds all
         pat = re.compile(r"\b((?:" + "|".join(map(re.escape, p.kernel_names)) + r")(?:_F)?)\b")

@@ -747,6 +747,54 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
 
   if (warp < PW) {
     const int p = threadIdx.x;  // 0..255
+    if constexpr (A_MN && F::VEC) {
+      // MN-major A, 4-pixel functor: lane owns tile pixels 4*lane .. 4*lane+3 (one
+      // 16 B chunk of a swizzled row), warp w owns k-rows w*ROWS .. (warp-uniform
+      // row context).  The functor shares its index math and addresses across the
+      // 4 pixels; stores are 16 B.  S % 4 == 0, so a quad never straddles images.
+      constexpr int ROWS = kBK / PW;
+      const long long tq = t0 + 4 * lane;
+      const bool okq = tq < T;
+      const int pn = okq ? (int)(tq / F::S) : 0;
+      const int ps = okq ? (int)(tq - (long long)pn * F::S) : 0;
+      float va[ROWS][4];
+      auto gather = [&](int kb) {
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+          const int k = kb * kBK + warp * ROWS + q;
+          const int kc = k < F::K ? k : F::K - 1;
+          const typename F::B4R R = F::B4row(a, kc);
+          F::B4k(a, R, (long long)pn, ps, va[q]);
+          const bool ok = okq && k < F::K;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            if constexpr (F::SAVE_B) {
+              if (ok) F::save_b(a, (long long)pn, k, ps + e, va[q][e]);
+            }
+            va[q][e] = ok ? va[q][e] : 0.f;
+          }
+        }
+      };
+      gather(0);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+        uint8_t* sa_hi = smem + st * L::STAGE;
+        uint8_t* sa_lo = sa_hi + L::A_BYTES;
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+          float h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) split_tf32(va[q][e], h[e], l[e]);
+          const int off = mn_off(4 * lane, warp * ROWS + q);
+          *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+        fence_async_smem();
+        mbar_arrive(&full[st]);
+        if (kb + 1 < KB) gather(kb + 1);
+      }
+    } else {
     if (A_MN) {
       // MN-major A: warp w owns k-rows 4w..4w+3 of the 32-wide k-block, lane =
       // pixel within each 32-pixel block (4 blocks).  k is warp-uniform, so the
@@ -882,6 +930,7 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       if (kb + 1 < KB) gather(kb + 1);
     }
     }
+    }
     // epilogue: TMEM lane quadrant = warp % 4, column half = warp / 4
     mbar_wait(done, 0);
     fence_after();
@@ -990,6 +1039,48 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
   const cv_u32 tmem = *tslot;
 
   if (warp < PW) {
+   if constexpr (F::VEC) {
+    // ---- producers, 4-pixel functor: lane owns tile pixels 4*lane .. 4*lane+3
+    long long g = 0;
+    for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x) {
+      const long long tq = (tile / NCT) * kBM + 4 * lane;
+      const bool okq = tq < T;
+      const int pn = okq ? (int)(tq / F::S) : 0;
+      const int ps = okq ? (int)(tq - (long long)pn * F::S) : 0;
+      float va[ROWS][4];
+      auto gather = [&](int kb) {
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+          const int k = kb * kBK + warp * ROWS + q;
+          const int kc = k < F::K ? k : F::K - 1;
+          const typename F::B4R R = F::B4row(a, kc);
+          F::B4k(a, R, (long long)pn, ps, va[q]);
+          const bool ok = okq && k < F::K;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) va[q][e] = ok ? va[q][e] : 0.f;
+        }
+      };
+      gather(0);
+      for (int kb = 0; kb < KB; ++kb, ++g) {
+        const int st = (int)(g % STAGES);
+        if (g >= STAGES) mbar_wait(&empty[st], (cv_u32)(((g / STAGES) & 1) ^ 1));
+        uint8_t* sa_hi = smem + st * L::STAGE;
+        uint8_t* sa_lo = sa_hi + L::A_BYTES;
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) {
+          float h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) split_tf32(va[q][e], h[e], l[e]);
+          const int off = mn_off(4 * lane, warp * ROWS + q);
+          *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+        fence_async_smem();
+        mbar_arrive(&full[st]);
+        if (kb + 1 < KB) gather(kb + 1);
+      }
+    }
+   } else {
     // ---- producers: MN-major computed operand, warp owns ROWS k-rows, lane = pixel
     long long g = 0;  // global k-block counter (ring position)
     for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x) {
@@ -1039,6 +1130,7 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
         if (kb + 1 < KB) gather(kb + 1);
       }
     }
+   }
   } else if (warp == PW) {
     // ---- MMA issuer
     if (lane == 0) {
@@ -1201,7 +1293,80 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   const int j0 = blockIdx.x * kBM * JG;  // rows: input channels (JG tiles of 128)
   const int m0 = blockIdx.y * NT;        // cols: output channels
 
+  if constexpr (F::VEC) if (warp < PW) {
+    // 4-pixel functors: lane = (row sub-index sub = lane / 8, pixel quad = lane % 8)
+    // — a warp covers 4 rows x 32 pixels per pass, each thread one 16 B swizzle
+    // chunk (4 consecutive pixels) of a row.  Row contexts are fixed for the CTA.
+    constexpr int RP = PW * 4;  // rows per pass
+    static_assert((kBM * JG) % RP == 0, "row passes must tile the 128-row MMA side");
+    constexpr int RA = kBM * JG / RP, RB = (NT + RP - 1) / RP;
+    const int quad = lane & 7, sub = lane >> 3;
+    typename F::B4R rb[RA];
+    typename F::A4R ra[RB];
+#pragma unroll
+    for (int w = 0; w < RA; ++w) {
+      const int jj = j0 + warp * 4 + sub + RP * w;
+      rb[w] = F::B4row(a, jj < F::J ? jj : F::J - 1);
+    }
+#pragma unroll
+    for (int w = 0; w < RB; ++w) {
+      const int mm = m0 + warp * 4 + sub + RP * w;
+      ra[w] = F::A4row(a, mm < F::M ? mm : F::M - 1);
+    }
+    float va[RA][4], vb[RB][4];
+    auto gather = [&](int kb) {
+      const long long t = tbeg + (long long)kb * kBK + 4 * quad;
+      const bool ok = t < tend;  // tend - tbeg is a multiple of 4 (S % 4 == 0)
+      const int ti = (int)(ok ? t : tbeg);
+      const int n = ti / F::S;
+      const int s = ti - n * F::S;
+#pragma unroll
+      for (int w = 0; w < RA; ++w) F::B4k(a, rb[w], (long long)n, s, va[w]);
+#pragma unroll
+      for (int w = 0; w < RB; ++w) {
+        F::A4k(a, ra[w], (long long)n, s, vb[w]);
+        const bool keep = ok && warp * 4 + sub + RP * w < NT;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) vb[w][e] = keep ? vb[w][e] : 0.f;
+      }
+    };
+    if (KB > 0) gather(0);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      uint8_t* sa_hi = smem + st * L::STAGE;
+      uint8_t* sa_lo = sa_hi + L::A_BYTES;
+      uint8_t* sb_hi = sa_lo + L::A_BYTES;
+      uint8_t* sb_lo = sb_hi + L::B_BYTES;
+#pragma unroll
+      for (int w = 0; w < RA; ++w) {
+        const int row = warp * 4 + sub + RP * w;
+        const int off = row * 128 + ((quad ^ (row & 7)) << 4);
+        float h[4], l[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) split_tf32(va[w][e], h[e], l[e]);
+        *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+#pragma unroll
+      for (int w = 0; w < RB; ++w) {
+        const int row = warp * 4 + sub + RP * w;
+        if (row < NT) {
+          const int off = row * 128 + ((quad ^ (row & 7)) << 4);
+          float h[4], l[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) split_tf32(vb[w][e], h[e], l[e]);
+          *reinterpret_cast<float4*>(sb_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+          *reinterpret_cast<float4*>(sb_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(&full[st]);
+      if (kb + 1 < KB) gather(kb + 1);
+    }
+  }
   if (warp < PW) {
+    if constexpr (!F::VEC) {
     // lane = pixel of the 32-pixel k-block (coalesced gathers, one pixel
     // decomposition per k-block); warp w owns rows w, w+8, ... (channel index
     // math is warp-uniform); each warp writes whole 128 B swizzled rows.
@@ -1286,6 +1451,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       mbar_arrive(&full[st]);
       prefetch(kb + 1 + kPfDist);
       if (kb + 1 < KB) gather(kb + 1);
+    }
     }
     mbar_wait(done, 0);
     fence_after();

@@ -71,6 +71,7 @@ TC_NTMAX = int(os.environ.get("CANVAS_TC_NTMAX", "256"))  # widest MMA N tile
 TC_PERSIST = os.environ.get("CANVAS_TC_PERSIST", "1") == "1"  # persistent fwd/dgrad GEMMs
 TC_PW = int(os.environ.get("CANVAS_TC_PW", "16"))  # producer warps of the persistent GEMM when K > 128 (16 vs 8: +0.4% img/s on config 2, no spills)
 SMS = 148
+VEC_PRODUCERS = os.environ.get("CANVAS_VEC", "1") == "1"  # tcgen05 producers evaluate 4 consecutive pixels per thread
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
 TC_WGRAD_JG_MAX = int(os.environ.get("CANVAS_WGRAD_JG", "1"))  # max row tiles per wgrad CTA (1 vs 2: +0.5% img/s on config 2 with 8192-pixel chunks)
@@ -275,6 +276,35 @@ _BC_FWD = {
 }
 
 
+class VecUnsupported(Exception):
+    """The functor body cannot be emitted in 4-pixel vector form (loops, caller-written
+    code, a pixel coordinate used non-affinely where the lanes would diverge)."""
+
+
+_TERM = re.compile(r"^\(?(-?\w+)\)?(?:\*\(?(-?\d+)\)?)?$")
+_MODDIV = re.compile(r"^(\w+) ([%/]) (\d+)$")
+
+
+def _split_top(expr: str, sep: str = " + ") -> list:
+    """Split ``expr`` on ``sep`` outside parentheses."""
+    out, depth, cur, i = [], 0, [], 0
+    while i < len(expr):
+        ch = expr[i]
+        if ch == "(":
+            depth += 1
+        elif ch == ")":
+            depth -= 1
+        if depth == 0 and expr.startswith(sep, i):
+            out.append("".join(cur))
+            cur = []
+            i += len(sep)
+            continue
+        cur.append(ch)
+        i += 1
+    out.append("".join(cur))
+    return out
+
+
 class Fn:
     """Straight-line code for one functor body with memoised coordinates/values.
 
@@ -313,10 +343,89 @@ class Fn:
         self.uni_lines: list[str] = []
         self.uni_vars: list[str] = []
         self.loaded: dict = {}  # (slot, image stride) -> TDesc of every tensor this functor reads
+        # vector mode (V > 1): the functor evaluates V consecutive pixels s0 .. s0+V-1
+        # (s0 a multiple of V, all in one image).  An int var in ``lanes`` holds its
+        # lane-0 value and lane e is var + coef*e (value (coef, align): lane-0 value is
+        # a multiple of align); a var in ``copies`` exists per lane as var_0 .. var_{V-1}.
+        # Everything else is lane-invariant and shared by the V pixels — the channel /
+        # tap / row index math, the image base, the row part of every address.
+        self.V = 1
+        self.lanes: dict = {}
+        self.copies: set = set()
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
+        if self.V > 1:
+            raise VecUnsupported(s)
+        self._emit(s)
+
+    def _emit(self, s: str) -> None:
         self.lines.append("  " * self.indent + s)
+
+    # -- vector mode ------------------------------------------------------------
+    def lane_vars(self, expr: str) -> set:
+        return {t for t in _IDENT.findall(expr) if t in self.lanes or t in self.copies}
+
+    def subst(self, expr: str, e: int) -> str:
+        """``expr`` at lane e."""
+
+        def rep(m):
+            t = m.group(0)
+            if t in self.copies:
+                return f"{t}_{e}"
+            if t in self.lanes and e:
+                return f"({t} + {self.lanes[t][0] * e})"
+            return t
+
+        return re.sub(r"\b[A-Za-z_]\w*\b", rep, expr)
+
+    def lane_affine(self, expr: str):
+        """(coef, align) when ``expr`` (which reads lane vars) is lane-affine with its
+        lane-0 value given by the expression itself; None when the lanes diverge."""
+        m = _MODDIV.match(expr)
+        if m:
+            x, op, q = m.group(1), m.group(2), int(m.group(3))
+            if x not in self.lanes:
+                return None
+            c, A = self.lanes[x]
+            # x0 % q + c*(V-1) < q and x0 / q shared by the lanes when the lane-0
+            # value is a multiple of A, A | q and the lanes stay inside one A block
+            if c > 0 and A % c == 0 and q % A == 0 and c * (self.V - 1) < A:
+                return (c, A) if op == "%" else (0, 0)
+            return None
+        coef, align = 0, 0
+        for t in _split_top(expr):
+            t = t.strip()
+            mt = _TERM.match(t)
+            if not mt:
+                return None
+            x, k = mt.group(1), int(mt.group(2)) if mt.group(2) else 1
+            if x.lstrip("-").isdigit():
+                align = math.gcd(align, int(x) * k)
+            elif x in self.copies:
+                return None
+            elif x in self.lanes:
+                c, A = self.lanes[x]
+                coef += c * k
+                align = math.gcd(align, A * k)
+            else:
+                align = math.gcd(align, k)
+        return coef, abs(align) if align else 1 << 20
+
+    def define(self, ctype: str, name: str, expr: str, aff=None) -> None:
+        """Emit ``ctype name = expr`` — per lane when expr reads lane vars (unless
+        ``aff`` = (coef, align) says it is lane-affine: then once, at lane 0)."""
+        if self.V > 1 and self.lane_vars(expr):
+            if aff is not None:
+                self._emit(f"{ctype} {name} = {expr};")
+                if aff[0]:
+                    self.lanes[name] = aff
+                return
+            for e in range(self.V):
+                self._emit(f"{ctype} {name}_{e} = {self.subst(expr, e)};")
+            self.copies.add(name)
+            return
+        self._emit(f"{ctype} {name} = {expr};")
 
     def fresh(self, p: str) -> str:
         self.k += 1
@@ -358,8 +467,11 @@ class Fn:
         if uni and self.hoist:
             self.uni_lines.append(f"const int {v} = {expr};")
             self.uni_vars.append(v)
+        elif self.V > 1 and self.lane_vars(expr):
+            aff = self.lane_affine(expr)
+            self.define("const int", v, expr, aff)
         else:
-            self.emit(f"const int {v} = {expr};")
+            self._emit(f"const int {v} = {expr};")
         self.memo_put(("i", expr), v)
         if uni:
             self.uniform.add(v)
@@ -371,7 +483,7 @@ class Fn:
         if got:
             return got
         v = self.fresh("v")
-        self.emit(f"const float {v} = {expr};")
+        self.define("const float", v, expr)
         self.memo_put(key, v)
         return v
 
@@ -478,9 +590,26 @@ class Fn:
         lp = self.memo_get(key)
         if not lp:
             lp = self.fresh("lp")
-            self.emit(f"float* const {lp} = {p} + {lane};")
+            if lane in self.lanes:  # vector mode, lane-affine: the lane-0 pointer (loads add coef*e)
+                self._emit(f"float* const {lp} = {p} + {lane};")
+            else:
+                self.define("float* const", lp, f"{p} + {lane}")
             self.memo_put(key, lp)
         return f"canvas::ptr_add({lp}, {uni})"
+
+    def vec_addr(self, d: TDesc, coords):
+        """Vector mode: (address, coef) — lane e reads address + coef*e — or
+        (address, None) when the lanes need their own addresses (substituted)."""
+        a = self.addr(d, coords)
+        lane, _ = self.offset_parts(d, coords)
+        _, nb = self.base(d)
+        if nb and "n" not in self.uniform and lane != "0":
+            lane = self.ivar(f"{nb} + {lane}")
+        if lane in self.lanes:
+            return a, self.lanes[lane][0]
+        if self.lane_vars(a):
+            return a, None
+        return a, 0
 
     def raw_ivar(self, expr: str) -> str:
         v = self.ivar(expr)
@@ -528,9 +657,30 @@ class Fn:
         # compiler can share it
         if any(str(c) in self.raw for c in coords):
             preds = self.guard + tuple(p for p in preds if p not in self.guard)
+        if self.V > 1:
+            return self._load_vec(d, coords, preds)
         if preds:
             return self.fvar(f"({' && '.join(preds)}) ? __ldg({self.addr(d, coords)}) : 0.f")
         return self.fvar(f"__ldg({self.addr(d, coords)})")
+
+    def _load_vec(self, d: TDesc, coords, preds) -> str:
+        a, c = self.vec_addr(d, coords)
+        pe = " && ".join(preds)
+        key = ("ldv", a, pe)
+        got = self.memo_get(key)
+        if got:
+            return got
+        if c == 0 and not (pe and self.lane_vars(pe)):
+            v = self.fvar(f"({pe}) ? __ldg({a}) : 0.f" if pe else f"__ldg({a})")  # lane-invariant
+        else:
+            v = self.fresh("v")
+            for e in range(self.V):
+                ae = f"{a} + {c * e}" if c is not None and c * e else (a if c is not None else self.subst(a, e))
+                pl = self.subst(pe, e) if pe else ""
+                self._emit(f"const float {v}_{e} = ({pl}) ? __ldg({ae}) : 0.f;" if pl else f"const float {v}_{e} = __ldg({ae});")
+            self.copies.add(v)
+        self.memo_put(key, v)
+        return v
 
     def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
         a = self.addr(d, coords)
@@ -1287,19 +1437,56 @@ class Lowerer:
         tcgen05 producers whose rows are fixed for a whole CTA (wgrad) build the
         row contexts once and pay only the per-pixel part per element;
         ``{name}(a, n, uvar, s)`` composes the two for the other templates."""
-        mem = f.uni_vars
-        out = [f"  struct {name}R {{ int {', '.join(mem) if mem else '_unused'}; }};"]
+        # the row variable itself travels in the context too: caller-written bodies
+        # (dense_conv.py) reference it directly
+        mem = [uvar + "_"] + list(f.uni_vars)
+        out = [f"  struct {name}R {{ int {', '.join(mem)}; }};"]
         out.append(f"  static __device__ __forceinline__ {name}R {name}row(const CanvasArgs& a, const int {uvar}) {{")
         out += ["    " + ln for ln in f.uni_lines]
         out.append(f"    {name}R R;")
-        out += [f"    R.{v} = {v};" for v in mem]
-        if not mem:
-            out.append("    R._unused = 0;")
+        out.append(f"    R.{uvar}_ = {uvar};")
+        out += [f"    R.{v} = {v};" for v in mem[1:]]
         out += ["    return R;", "  }"]
         out.append(f"  static __device__ __forceinline__ float {name}k(const CanvasArgs& a, const {name}R& R, const long long n, const int s) {{")
-        out += [f"    const int {v} = R.{v};" for v in mem]
+        out.append(f"    const int {uvar} = R.{uvar}_; (void){uvar};")
+        out += [f"    const int {v} = R.{v};" for v in mem[1:]]
         out += ["    " + ln for ln in f.pre] + f.lines + [f"    return {val};", "  }"]
         out.append(f"  static __device__ __forceinline__ float {name}(const CanvasArgs& a, const long long n, const int {uvar}, const int s) {{ return {name}k(a, {name}row(a, {uvar}), n, s); }}")
+        return out
+
+    def vec_operand(self, name: str, fn, uvar: str, S: int, local_slots: list) -> list:
+        """4-pixel form of an operand functor (Fn vector mode): ``{name}R`` /
+        ``{name}row(a, uvar)`` (its own row context) and ``{name}k(a, R, n, s, o)``
+        writing pixels s .. s+3 (s a multiple of 4) to o[0..3].  The lane-invariant
+        index math (channel / tap decomposition, image base, row offsets, the pixel's
+        (h, w) split when W % 4 == 0) runs once per 4 pixels and lane-affine loads
+        share one address (immediate offsets).  [] when S % 4 != 0 or the body is
+        not vectorisable (the template then keeps the scalar producer)."""
+        if not VEC_PRODUCERS or S % 4:
+            return []
+        f = Fn(self)
+        f.pre = []
+        f.computing = None
+        f.local_slots = local_slots
+        f.uniform = {uvar}
+        f.hoist = True
+        f.V = 4
+        f.lanes = {"s": (1, 4)}
+        try:
+            val = fn(f)
+        except VecUnsupported:
+            return []
+        mem = [uvar + "_"] + list(f.uni_vars)
+        out = [f"  struct {name}R {{ int {', '.join(mem)}; }};"]
+        out.append(f"  static __device__ __forceinline__ {name}R {name}row(const CanvasArgs& a, const int {uvar}) {{")
+        out += ["    " + ln for ln in f.uni_lines]
+        out += [f"    {name}R R;", f"    R.{uvar}_ = {uvar};"] + [f"    R.{v} = {v};" for v in mem[1:]] + ["    return R;", "  }"]
+        out.append(f"  static __device__ __forceinline__ void {name}k(const CanvasArgs& a, const {name}R& R, const long long n, const int s, float* o) {{")
+        out.append(f"    const int {uvar} = R.{uvar}_; (void){uvar};")
+        out += [f"    const int {v} = R.{v};" for v in mem[1:]]
+        out += ["    " + ln for ln in f.pre] + f.lines
+        out += [f"    o[{e}] = {val + '_' + str(e) if val in f.copies else val};" for e in range(4)]
+        out.append("  }")
         return out
 
     @staticmethod
@@ -1354,6 +1541,8 @@ class Lowerer:
             "  }",
         ]
         lines += self.split_operand("B", fb, bval, "k")
+        vec = self.vec_operand("B4", bfn, "k", S, fa.local_slots)
+        lines += vec + [f"  static constexpr bool VEC = {'true' if vec else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
         tc = self.use_tc and M >= 8 and K >= 16
@@ -1462,6 +1651,10 @@ class Lowerer:
         ]
         lines += self.split_operand("A", fa, aval, "m")
         lines += self.split_operand("B", fb, bval, "k")
+        va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots)
+        vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots) if va4 else []
+        lines += (va4 + vb4) if vb4 else []
+        lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'};"]
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
         lines += self.prefetch_members(fa, [fb, fa], S)
         lines += ["};"]

@@ -122,12 +122,72 @@ void reduce_partials(const CanvasArgs& a) {
     a.p[1][F::TJ > 0 ? (idx % F::TJ) * (F::MJ / F::TJ) + idx / F::TJ : idx] = s;
   }
 }
+// 4-pixel operand functors (F::VEC): the tcgen05 producers call B4row/B4k
+// (A4row/A4k) on pixel quads; the emulation evaluates the operands the same way
+template <class F>
+void gemm_nk_vec(const CanvasArgs& a) {
+  const long long T = a.n * (long long)F::S;
+  float* col = new float[4 * F::K];
+  for (long long t = 0; t < T; t += 4) {
+    const long long n = t / F::S;
+    const int s = (int)(t - n * F::S);
+    for (int k = 0; k < F::K; ++k) {
+      const typename F::B4R R = F::B4row(a, k);
+      F::B4k(a, R, n, s, col + 4 * k);
+      if constexpr (F::SAVE_B)
+        for (int e = 0; e < 4; ++e) F::save_b(a, n, k, s + e, col[4 * k + e]);
+    }
+    for (int e = 0; e < 4; ++e)
+      for (int m = 0; m < F::M; ++m) {
+        float acc = 0.f;
+        for (int k = 0; k < F::K; ++k) acc = std::fma(F::A(a, m, k), col[4 * k + e], acc);
+        F::store(a, n, m, s + e, acc);
+      }
+  }
+  delete[] col;
+}
+
+template <class F>
+void gemm_wgrad_vec(const CanvasArgs& a) {
+  const long long T = a.n * (long long)F::S;
+  const long long Z = (T + F::TCHUNK - 1) / F::TCHUNK;
+  float* av = new float[4 * F::M];
+  float* bv = new float[4 * F::J];
+  for (long long z = 0; z < Z; ++z) {
+    float* P = F::partials(a) + z * F::M * F::J;
+    std::memset(P, 0, sizeof(float) * F::M * F::J);
+    const long long te = std::min<long long>((z + 1) * F::TCHUNK, T);
+    for (long long t = z * F::TCHUNK; t < te; t += 4) {
+      const long long n = t / F::S;
+      const int s = (int)(t - n * F::S);
+      for (int m = 0; m < F::M; ++m) F::A4k(a, F::A4row(a, m), n, s, av + 4 * m);
+      for (int j = 0; j < F::J; ++j) F::B4k(a, F::B4row(a, j), n, s, bv + 4 * j);
+      for (int e = 0; e < 4; ++e)
+        for (int m = 0; m < F::M; ++m)
+          for (int j = 0; j < F::J; ++j) P[m * F::J + j] = std::fma(av[4 * m + e], bv[4 * j + e], P[m * F::J + j]);
+    }
+  }
+  delete[] av;
+  delete[] bv;
+}
+
+template <class F>
+void gemm_nk_tc(const CanvasArgs& a) {
+  if constexpr (F::VEC) gemm_nk_vec<F>(a);
+  else gemm_nk<F>(a);
+}
+template <class F>
+void gemm_wgrad_tc(const CanvasArgs& a) {
+  if constexpr (F::VEC) gemm_wgrad_vec<F>(a);
+  else gemm_wgrad<F>(a);
+}
+
 template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = 8, int NACC = 1>
-void tc_gemm_pix(const CanvasArgs& a) { gemm_nk<F>(a); }
+void tc_gemm_pix(const CanvasArgs& a) { gemm_nk_tc<F>(a); }
 template <class F, int NT>
 void tc_pack_b(const CanvasArgs&) {}
 template <class F, int NT, int STAGES, int PW, int EW>
-void tc_gemm_pix_persistent(const CanvasArgs& a) { gemm_nk<F>(a); }
+void tc_gemm_pix_persistent(const CanvasArgs& a) { gemm_nk_tc<F>(a); }
 template <class F, int NT, int STAGES, int PW = 8, int JG = 1>
-void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad<F>(a); }
+void tc_gemm_wgrad(const CanvasArgs& a) { gemm_wgrad_tc<F>(a); }
 }  // namespace canvas

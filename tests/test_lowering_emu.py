@@ -31,6 +31,18 @@ def test_pinned(name):
     assert_close(case, *emu_run(case), name)
 
 
+@pytest.mark.parametrize("h,w", [(6, 12), (6, 14), (7, 4)])
+@pytest.mark.parametrize("name", ["seed7_k1", "involution", "im2col", "seed7_k0"])
+def test_vector_producers(name, h, w):
+    """S % 4 == 0: the tcgen05 operand functors are emitted in 4-pixel form (W % 4
+    == 0: lane-affine pixel coordinates; W = 14: per-lane (h, w) copies) and the
+    emulated GEMMs evaluate them on pixel quads."""
+    case = reference(zoo.ALL[name], 16, 16, h, w)
+    if name != "seed7_k0":  # seed-7 #0 has no FC
+        assert "static constexpr bool VEC = true;" in case.plan.source
+    assert_close(case, *emu_run(case), f"{name} vec {h}x{w}")
+
+
 @pytest.mark.parametrize("cin,cout,stride", [(8, 16, 2), (16, 8, 1), (8, 32, 2)])
 @pytest.mark.parametrize("name", ["seed7_k1", "involution", "seed7_k0"])
 def test_replication(name, cin, cout, stride):
