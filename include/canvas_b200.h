@@ -74,7 +74,10 @@ int canvas_plan_query(const canvas_plan* p, int64_t batch, size_t* fwd_workspace
 int canvas_plan_launches(const canvas_plan* p, int phase);
 
 /* y = kernel(x) for every Fig.-2 replica.  fc_w holds n_fc device pointers
- * (replica-major, IR edge order, each [out, prod(in ch)] row-major). */
+ * (replica-major, IR edge order, each [out, prod(in ch)] row-major).
+ * Launch records of blob kind 2 issue 16-byte vector accesses: every tensor
+ * pointer they receive must be 16-byte aligned (CANVAS_ERR_ARGS otherwise;
+ * PyTorch allocations always are). */
 int canvas_forward(const canvas_plan* p, int64_t batch, const float* x, const float* const* fc_w, int n_fc,
                    float* y, void* saved, void* workspace, void* stream);
 

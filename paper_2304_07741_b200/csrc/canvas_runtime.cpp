@@ -399,8 +399,14 @@ int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, co
       }
       CanvasArgs a;
       std::memset(&a, 0, sizeof(a));
-      for (int64_t i = 0; i < r.nslots; ++i)
+      for (int64_t i = 0; i < r.nslots; ++i) {
         a.p[i] = slot_ptr(p, r.slots[i], copy, batch, x, w, y, dy, dx, dw, saved, ws);
+        // kind 2: the kernel's 4-element quads are 16 B loads / stores
+        if (r.kind == 2 && ((uintptr_t)a.p[i] & 15u) != 0)
+          return fail(CANVAS_ERR_ARGS, "tensor pointer of slot " + std::to_string(r.slots[i]) + " (copy " +
+                                           std::to_string(copy) + ") is not 16-byte aligned; launch " +
+                                           std::to_string(&r - p->recs.data()) + " uses 16 B accesses");
+      }
       a.n = batch;
       a.beta = (r.beta == 2) || (r.beta == 1 && copy > 0);
       a.copy = (int)copy;
@@ -498,7 +504,7 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
     r.beta = rd.i64();
     r.memset_slot = rd.i64();
     r.memset_size = SizeRule{rd.i64(), rd.i64(), rd.i64()};
-    if (!rd.ok || r.nslots < 0 || r.nslots > kMaxSlots || (r.kind == 0 && (r.kernel < 0 || r.kernel >= n_kernels)))
+    if (!rd.ok || r.nslots < 0 || r.nslots > kMaxSlots || (r.kind != 1 && (r.kernel < 0 || r.kernel >= n_kernels)) || r.kind < 0 || r.kind > 2)
       return fail(CANVAS_ERR_BLOB, "bad launch record " + std::to_string(i));
     for (const auto& g : r.grid)
       if (g.d <= 0) return fail(CANVAS_ERR_BLOB, "bad grid rule");
@@ -544,7 +550,7 @@ int canvas_plan_create(const void* blob, size_t nbytes, int cuda_device, canvas_
     p->fns.push_back(f);
   }
   for (const Record& r : p->recs) {
-    if (r.kind == 0 && r.smem > 48 * 1024) {
+    if (r.kind != 1 && r.smem > 48 * 1024) {
       e = d.cuFuncSetAttribute(p->fns[r.kernel], 8 /* MAX_DYNAMIC_SHARED_SIZE_BYTES */, (int)r.smem);
       if (e != 0) return fail(CANVAS_ERR_CUDA, "cuFuncSetAttribute(smem " + std::to_string(r.smem) + "): " + cu_err(e));
     }
@@ -571,7 +577,7 @@ int canvas_plan_launches(const canvas_plan* p, int phase) {
   if (!p) return fail(CANVAS_ERR_ARGS, "null plan");
   int n = 0;
   for (const auto& r : p->recs)
-    if (r.phase == phase && r.kind == 0) n += (int)p->copies;
+    if (r.phase == phase && r.kind != 1) n += (int)p->copies;
   return n;
 }
 

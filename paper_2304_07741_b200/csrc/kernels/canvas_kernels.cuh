@@ -98,6 +98,31 @@ __device__ __forceinline__ void pointwise_planes(const CanvasArgs& a) {
   }
 }
 
+// 4-element variants: each thread evaluates the 4 consecutive elements r .. r+3
+// (F::run4; PER, resp. S, is a multiple of 4 so a quad stays in one image /
+// plane).  The functor computes the lane-invariant part of its index math
+// (channel / tap decomposition, replica loop bounds, row offsets) once per quad
+// and issues each lane-affine gather from one address with immediate offsets.
+template <class F>
+__device__ __forceinline__ void pointwise4(const CanvasArgs& a) {
+  const long long total = a.n * F::PER;
+  for (long long i = 4 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); i < total; i += 4LL * gridDim.x * blockDim.x) {
+    const long long n = i / F::PER;
+    F::run4(a, n, (int)(i - n * F::PER));
+  }
+}
+
+template <class F>
+__device__ __forceinline__ void pointwise_planes4(const CanvasArgs& a) {
+  const long long planes = a.n * F::Q;
+  const int s = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
+  for (long long pq = blockIdx.y; pq < planes; pq += gridDim.y) {
+    const long long n = pq / F::Q;
+    const int q = (int)(pq - n * F::Q);
+    if (s < F::S) F::run4(a, n, q, s);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2: softmax / row-dot over a channel span with SL threads per row.  When
 // rows are few and long (ResNet stage 4: 49 pixels x 512 channels) a thread
@@ -757,42 +782,68 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       const bool okq = tq < T;
       const int pn = okq ? (int)(tq / F::S) : 0;
       const int ps = okq ? (int)(tq - (long long)pn * F::S) : 0;
-      float va[ROWS][4];
-      auto gather = [&](int kb) {
-#pragma unroll
-        for (int q = 0; q < ROWS; ++q) {
-          const int k = kb * kBK + warp * ROWS + q;
-          const int kc = k < F::K ? k : F::K - 1;
-          const typename F::B4R R = F::B4row(a, kc);
-          F::B4k(a, R, (long long)pn, ps, va[q]);
-          const bool ok = okq && k < F::K;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            if constexpr (F::SAVE_B) {
-              if (ok) F::save_b(a, (long long)pn, k, ps + e, va[q][e]);
-            }
-            va[q][e] = ok ? va[q][e] : 0.f;
-          }
-        }
-      };
-      gather(0);
-      for (int kb = 0; kb < KB; ++kb) {
+      auto put = [&](int kb, float (&va)[ROWS][4]) {
         const int st = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
         uint8_t* sa_hi = smem + st * L::STAGE;
         uint8_t* sa_lo = sa_hi + L::A_BYTES;
 #pragma unroll
         for (int q = 0; q < ROWS; ++q) {
+          const int k = kb * kBK + warp * ROWS + q;
+          const bool ok = okq && k < F::K;
           float h[4], l[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) split_tf32(va[q][e], h[e], l[e]);
+          for (int e = 0; e < 4; ++e) {
+            if constexpr (F::SAVE_B) {
+              if (ok) F::save_b(a, (long long)pn, k, ps + e, va[q][e]);
+            }
+            split_tf32(ok ? va[q][e] : 0.f, h[e], l[e]);
+          }
           const int off = mn_off(4 * lane, warp * ROWS + q);
           *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
           *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
         }
         fence_async_smem();
         mbar_arrive(&full[st]);
-        if (kb + 1 < KB) gather(kb + 1);
+      };
+      auto row = [&](int kb, int q) {
+        const int k = kb * kBK + warp * ROWS + q;
+        return F::B4row(a, k < F::K ? k : F::K - 1);
+      };
+      if constexpr (F::SPLIT) {
+        // software pipeline: k-block kb+1's gathers are in flight while kb is combined and stored
+        constexpr int NB = F::B4NRAW;
+        float x0[ROWS][NB], x1[ROWS][NB];
+        auto issue = [&](int kb, float (&x)[ROWS][NB]) {
+#pragma unroll
+          for (int q = 0; q < ROWS; ++q) F::B4ld(a, row(kb, q), (long long)pn, ps, x[q]);
+        };
+        auto commit_kb = [&](int kb, const float (&x)[ROWS][NB]) {
+          float va[ROWS][4];
+#pragma unroll
+          for (int q = 0; q < ROWS; ++q) F::B4cp(a, row(kb, q), x[q], va[q]);
+          put(kb, va);
+        };
+        issue(0, x0);
+        for (int kb = 0; kb < KB; kb += 2) {
+          if (kb + 1 < KB) issue(kb + 1, x1);
+          commit_kb(kb, x0);
+          if (kb + 1 < KB) {
+            if (kb + 2 < KB) issue(kb + 2, x0);
+            commit_kb(kb + 1, x1);
+          }
+        }
+      } else {
+        float va[ROWS][4];
+        auto gather = [&](int kb) {
+#pragma unroll
+          for (int q = 0; q < ROWS; ++q) F::B4k(a, row(kb, q), (long long)pn, ps, va[q]);
+        };
+        gather(0);
+        for (int kb = 0; kb < KB; ++kb) {
+          put(kb, va);
+          if (kb + 1 < KB) gather(kb + 1);
+        }
       }
     } else {
     if (A_MN) {
@@ -1040,44 +1091,77 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
 
   if (warp < PW) {
    if constexpr (F::VEC) {
-    // ---- producers, 4-pixel functor: lane owns tile pixels 4*lane .. 4*lane+3
-    long long g = 0;
-    for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x) {
+    // ---- producers, 4-pixel functor: lane owns tile pixels 4*lane .. 4*lane+3.
+    // The CTA's (tile, k-block) work is one sequence g = 0 .. NG-1 (ring position g).
+    const long long my_tiles = blockIdx.x < TILES ? (TILES - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const long long NG = my_tiles * KB;
+    struct Pix {
+      int kb, pn, ps;
+      bool ok;
+    };
+    auto pix = [&](long long g) {
+      Pix P;
+      const long long tile = blockIdx.x + (g / KB) * gridDim.x;
+      P.kb = (int)(g % KB);
       const long long tq = (tile / NCT) * kBM + 4 * lane;
-      const bool okq = tq < T;
-      const int pn = okq ? (int)(tq / F::S) : 0;
-      const int ps = okq ? (int)(tq - (long long)pn * F::S) : 0;
-      float va[ROWS][4];
-      auto gather = [&](int kb) {
+      P.ok = tq < T;
+      P.pn = P.ok ? (int)(tq / F::S) : 0;
+      P.ps = P.ok ? (int)(tq - (long long)P.pn * F::S) : 0;
+      return P;
+    };
+    auto row = [&](int kb, int q) {
+      const int k = kb * kBK + warp * ROWS + q;
+      return F::B4row(a, k < F::K ? k : F::K - 1);
+    };
+    auto put = [&](long long g, const Pix& P, float (&va)[ROWS][4]) {
+      const int st = (int)(g % STAGES);
+      if (g >= STAGES) mbar_wait(&empty[st], (cv_u32)(((g / STAGES) & 1) ^ 1));
+      uint8_t* sa_hi = smem + st * L::STAGE;
+      uint8_t* sa_lo = sa_hi + L::A_BYTES;
 #pragma unroll
-        for (int q = 0; q < ROWS; ++q) {
-          const int k = kb * kBK + warp * ROWS + q;
-          const int kc = k < F::K ? k : F::K - 1;
-          const typename F::B4R R = F::B4row(a, kc);
-          F::B4k(a, R, (long long)pn, ps, va[q]);
-          const bool ok = okq && k < F::K;
+      for (int q = 0; q < ROWS; ++q) {
+        const bool ok = P.ok && P.kb * kBK + warp * ROWS + q < F::K;
+        float h[4], l[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) va[q][e] = ok ? va[q][e] : 0.f;
-        }
+        for (int e = 0; e < 4; ++e) split_tf32(ok ? va[q][e] : 0.f, h[e], l[e]);
+        const int off = mn_off(4 * lane, warp * ROWS + q);
+        *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+      }
+      fence_async_smem();
+      mbar_arrive(&full[st]);
+    };
+    if constexpr (F::SPLIT) {
+      constexpr int NB = F::B4NRAW;
+      float x0[ROWS][NB], x1[ROWS][NB];
+      Pix P0, P1;
+      auto issue = [&](long long g, float (&x)[ROWS][NB], Pix& P) {
+        P = pix(g);
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) F::B4ld(a, row(P.kb, q), (long long)P.pn, P.ps, x[q]);
       };
-      gather(0);
-      for (int kb = 0; kb < KB; ++kb, ++g) {
-        const int st = (int)(g % STAGES);
-        if (g >= STAGES) mbar_wait(&empty[st], (cv_u32)(((g / STAGES) & 1) ^ 1));
-        uint8_t* sa_hi = smem + st * L::STAGE;
-        uint8_t* sa_lo = sa_hi + L::A_BYTES;
+      auto commit_g = [&](long long g, const float (&x)[ROWS][NB], const Pix& P) {
+        float va[ROWS][4];
 #pragma unroll
-        for (int q = 0; q < ROWS; ++q) {
-          float h[4], l[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) split_tf32(va[q][e], h[e], l[e]);
-          const int off = mn_off(4 * lane, warp * ROWS + q);
-          *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<float4*>(sa_lo + off) = make_float4(l[0], l[1], l[2], l[3]);
+        for (int q = 0; q < ROWS; ++q) F::B4cp(a, row(P.kb, q), x[q], va[q]);
+        put(g, P, va);
+      };
+      if (NG > 0) issue(0, x0, P0);
+      for (long long g = 0; g < NG; g += 2) {
+        if (g + 1 < NG) issue(g + 1, x1, P1);
+        commit_g(g, x0, P0);
+        if (g + 1 < NG) {
+          if (g + 2 < NG) issue(g + 2, x0, P0);
+          commit_g(g + 1, x1, P1);
         }
-        fence_async_smem();
-        mbar_arrive(&full[st]);
-        if (kb + 1 < KB) gather(kb + 1);
+      }
+    } else {
+      for (long long g = 0; g < NG; ++g) {
+        const Pix P = pix(g);
+        float va[ROWS][4];
+#pragma unroll
+        for (int q = 0; q < ROWS; ++q) F::B4k(a, row(P.kb, q), (long long)P.pn, P.ps, va[q]);
+        put(g, P, va);
       }
     }
    } else {
@@ -1313,25 +1397,8 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       const int mm = m0 + warp * 4 + sub + RP * w;
       ra[w] = F::A4row(a, mm < F::M ? mm : F::M - 1);
     }
-    float va[RA][4], vb[RB][4];
-    auto gather = [&](int kb) {
-      const long long t = tbeg + (long long)kb * kBK + 4 * quad;
-      const bool ok = t < tend;  // tend - tbeg is a multiple of 4 (S % 4 == 0)
-      const int ti = (int)(ok ? t : tbeg);
-      const int n = ti / F::S;
-      const int s = ti - n * F::S;
-#pragma unroll
-      for (int w = 0; w < RA; ++w) F::B4k(a, rb[w], (long long)n, s, va[w]);
-#pragma unroll
-      for (int w = 0; w < RB; ++w) {
-        F::A4k(a, ra[w], (long long)n, s, vb[w]);
-        const bool keep = ok && warp * 4 + sub + RP * w < NT;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) vb[w][e] = keep ? vb[w][e] : 0.f;
-      }
-    };
-    if (KB > 0) gather(0);
-    for (int kb = 0; kb < KB; ++kb) {
+    // split-precision stores of one k-block's operand quads into ring slot kb % STAGES
+    auto put = [&](int kb, const float (&va)[RA][4], const float (&vb)[RB][4]) {
       const int st = kb % STAGES;
       if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
       uint8_t* sa_hi = smem + st * L::STAGE;
@@ -1362,7 +1429,71 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       }
       fence_async_smem();
       mbar_arrive(&full[st]);
-      if (kb + 1 < KB) gather(kb + 1);
+    };
+    auto pixel = [&](int kb, bool& ok, int& n, int& s) {
+      const long long t = tbeg + (long long)kb * kBK + 4 * quad;
+      ok = t < tend;  // tend - tbeg is a multiple of 4 (S % 4 == 0)
+      const int ti = (int)(ok ? t : tbeg);
+      n = ti / F::S;
+      s = ti - n * F::S;
+    };
+    if constexpr (F::SPLIT) {
+      // software pipeline: the gathers of k-block kb+1 (raw registers, no use)
+      // are issued before k-block kb is combined, split and stored
+      constexpr int NB = F::B4NRAW, NA = F::A4NRAW;
+      float xb0[RA][NB], xa0[RB][NA], xb1[RA][NB], xa1[RB][NA];
+      bool ok0 = false, ok1 = false;
+      auto issue = [&](int kb, float (&xb)[RA][NB], float (&xa)[RB][NA], bool& okv) {
+        int n, s;
+        pixel(kb, okv, n, s);
+#pragma unroll
+        for (int w = 0; w < RA; ++w) F::B4ld(a, rb[w], (long long)n, s, xb[w]);
+#pragma unroll
+        for (int w = 0; w < RB; ++w) F::A4ld(a, ra[w], (long long)n, s, xa[w]);
+      };
+      auto commit_kb = [&](int kb, const float (&xb)[RA][NB], const float (&xa)[RB][NA], bool okv) {
+        float va[RA][4], vb[RB][4];
+#pragma unroll
+        for (int w = 0; w < RA; ++w) F::B4cp(a, rb[w], xb[w], va[w]);
+#pragma unroll
+        for (int w = 0; w < RB; ++w) {
+          F::A4cp(a, ra[w], xa[w], vb[w]);
+          const bool keep = okv && warp * 4 + sub + RP * w < NT;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) vb[w][e] = keep ? vb[w][e] : 0.f;
+        }
+        put(kb, va, vb);
+      };
+      if (KB > 0) issue(0, xb0, xa0, ok0);
+      for (int kb = 0; kb < KB; kb += 2) {
+        if (kb + 1 < KB) issue(kb + 1, xb1, xa1, ok1);
+        commit_kb(kb, xb0, xa0, ok0);
+        if (kb + 1 < KB) {
+          if (kb + 2 < KB) issue(kb + 2, xb0, xa0, ok0);
+          commit_kb(kb + 1, xb1, xa1, ok1);
+        }
+      }
+    } else {
+      float va[RA][4], vb[RB][4];
+      auto gather = [&](int kb) {
+        bool ok;
+        int n, s;
+        pixel(kb, ok, n, s);
+#pragma unroll
+        for (int w = 0; w < RA; ++w) F::B4k(a, rb[w], (long long)n, s, va[w]);
+#pragma unroll
+        for (int w = 0; w < RB; ++w) {
+          F::A4k(a, ra[w], (long long)n, s, vb[w]);
+          const bool keep = ok && warp * 4 + sub + RP * w < NT;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) vb[w][e] = keep ? vb[w][e] : 0.f;
+        }
+      };
+      if (KB > 0) gather(0);
+      for (int kb = 0; kb < KB; ++kb) {
+        put(kb, va, vb);
+        if (kb + 1 < KB) gather(kb + 1);
+      }
     }
   }
   if (warp < PW) {

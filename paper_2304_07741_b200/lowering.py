@@ -72,6 +72,10 @@ TC_PERSIST = os.environ.get("CANVAS_TC_PERSIST", "1") == "1"  # persistent fwd/d
 TC_PW = int(os.environ.get("CANVAS_TC_PW", "16"))  # producer warps of the persistent GEMM when K > 128 (16 vs 8: +0.4% img/s on config 2, no spills)
 SMS = 148
 VEC_PRODUCERS = os.environ.get("CANVAS_VEC", "1") == "1"  # tcgen05 producers evaluate 4 consecutive pixels per thread
+VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launches: 4 consecutive elements per thread
+VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
+VEC_RT = os.environ.get("CANVAS_VEC_RT", "0") == "1"  # quads at a run-time 4 B offset: two 16 B loads + select (measured 1.7x slower on the layer1 GEMMs: off)
+VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
 TC_WGRAD_JG_MAX = int(os.environ.get("CANVAS_WGRAD_JG", "1"))  # max row tiles per wgrad CTA (1 vs 2: +0.5% img/s on config 2 with 8192-pixel chunks)
@@ -174,6 +178,7 @@ class Launch:
     what: str = ""  # human-readable role (profiles / DESIGN tables)
     bytes_per_image: int = 0  # algorithmic HBM bytes per image (roofline)
     flops_per_image: int = 0  # useful FLOPs per image (2 per MAC)
+    align16: bool = False  # the kernel issues 16 B accesses: the runtime checks slot pointers (blob kind 2)
 
 
 @dataclass
@@ -238,7 +243,7 @@ class Plan:
             grid = list(L.grid) if L.grid else [GridRule(0, 1, 1)] * 3
             slots = list(L.slots) + [-1] * (MAX_KSLOTS - len(L.slots))
             ms = L.memset_size or SizeRule(0, 1, 0)
-            out += struct.pack("<5q", 0 if L.kind == "kernel" else 1, L.phase, L.kernel, L.block, L.smem)
+            out += struct.pack("<5q", (2 if L.align16 else 0) if L.kind == "kernel" else 1, L.phase, L.kernel, L.block, L.smem)
             for g in grid:
                 out += struct.pack("<4q", g.a, g.b, g.d, g.cap)
             out += struct.pack("<q", len(L.slots))
@@ -352,15 +357,54 @@ class Fn:
         self.V = 1
         self.lanes: dict = {}
         self.copies: set = set()
+        # element alignment of int vars (their value is a multiple of it; lane-0 value
+        # for lane vars): lane-affine unit-stride accesses whose offset is a multiple
+        # of 4 become one 16 B access (slot pointers are 16 B aligned: launch kind 2)
+        self.al: dict = {}
+        self.vec16 = False
+        self.ltags: list = []
+        self.cur_tag = None
+        self.nld = {"aligned": 0, "shifted": 0, "lanes": 0}  # vector-mode load sites by kind
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
-        if self.V > 1:
+        """Emit a caller-written statement.  Vector mode: mutable float declarations
+        (accumulators, register rows) and statements that read lane values are
+        emitted once per lane with the lane's names substituted; lane-invariant
+        statements (loop headers, braces) once.  Caller-written ``const``
+        bindings are refused (their names would collide across lanes)."""
+        if self.V == 1:
+            self._emit(s)
+            return
+        st = s.strip()
+        if st.startswith("const "):
             raise VecUnsupported(s)
-        self._emit(s)
+        if st.startswith("float "):
+            body = st[len("float "):].rstrip(";").replace("; float ", ", ")
+            for decl in _split_top(body, ", "):
+                self.copies.add(re.match(r"\s*(\w+)", decl).group(1))
+        elif not self.lane_vars(s):
+            self._emit(s)
+            return
+        if s.count("{") != s.count("}"):
+            raise VecUnsupported(s)
+        for e in range(self.V):
+            self._emit(self.subst(s, e))
 
     def _emit(self, s: str) -> None:
         self.lines.append("  " * self.indent + s)
+        # line kinds for the load / compute split of operand functors: 'i' index
+        # math and addresses, 'l' loads, 'c' float arithmetic, 'x' anything else
+        st = s.lstrip()
+        if self.cur_tag:
+            tag = self.cur_tag
+        elif st.startswith(("const int ", "float* const ", "const float* const ")):
+            tag = "i"
+        elif st.startswith("const float ") and "__ldg" not in st:
+            tag = "c"
+        else:
+            tag = "x"
+        self.ltags.append(tag)
 
     # -- vector mode ------------------------------------------------------------
     def lane_vars(self, expr: str) -> set:
@@ -379,38 +423,71 @@ class Fn:
 
         return re.sub(r"\b[A-Za-z_]\w*\b", rep, expr)
 
-    def lane_affine(self, expr: str):
-        """(coef, align) when ``expr`` (which reads lane vars) is lane-affine with its
-        lane-0 value given by the expression itself; None when the lanes diverge."""
+    # residue classes (A, c): the value is = c (mod A); A = 0 means exactly c
+    @staticmethod
+    def _radd(x, y):
+        g = math.gcd(x[0], y[0])
+        return (g, (x[1] + y[1]) % g if g else x[1] + y[1])
+
+    @staticmethod
+    def _rmul(x, k: int):
+        return (abs(x[0] * k), (x[1] * k) % abs(x[0] * k) if x[0] * k else x[1] * k)
+
+    def residue(self, x: str):
+        x = x.strip()
+        if x.lstrip("-").isdigit():
+            return (0, int(x))
+        if x in self.lanes:
+            return self.lanes[x][1:]
+        return self.al.get(x, (1, 0))
+
+    def affine_info(self, expr: str):
+        """(lane coef, A, c) of an int expression — its (lane-0) value is = c mod A —
+        or None when it is not affine in the lanes (per-lane copies needed)."""
         m = _MODDIV.match(expr)
         if m:
             x, op, q = m.group(1), m.group(2), int(m.group(3))
-            if x not in self.lanes:
+            if x in self.copies:
                 return None
-            c, A = self.lanes[x]
-            # x0 % q + c*(V-1) < q and x0 / q shared by the lanes when the lane-0
-            # value is a multiple of A, A | q and the lanes stay inside one A block
-            if c > 0 and A % c == 0 and q % A == 0 and c * (self.V - 1) < A:
-                return (c, A) if op == "%" else (0, 0)
+            A, c = self.residue(x)
+            if x not in self.lanes:
+                if op == "%":
+                    g = math.gcd(A, q)
+                    return (0, g, c % g) if g else (0, 0, c % q)
+                return (0, 0, c // q) if A == 0 else (0, 1, 0)
+            cf = self.lanes[x][0]
+            # x0 % q + cf*(V-1) < q and x0 / q shared by the lanes when the lane-0
+            # value is = c mod A with A | q and c + cf*(V-1) < A (lanes stay in one A block)
+            if cf > 0 and A and q % A == 0 and c + cf * (self.V - 1) < A:
+                return (cf, A, c) if op == "%" else (0, 1, 0)
             return None
-        coef, align = 0, 0
+        coef, res = 0, (0, 0)
         for t in _split_top(expr):
             t = t.strip()
             mt = _TERM.match(t)
             if not mt:
-                return None
+                mp = re.match(r"^\((.*)\)\*\(?(-?\d+)\)?$", t)
+                if not mp:
+                    return None
+                inner = self.affine_info(mp.group(1))
+                if inner is None:
+                    return None
+                k = int(mp.group(2))
+                coef += inner[0] * k
+                res = self._radd(res, self._rmul(inner[1:], k))
+                continue
             x, k = mt.group(1), int(mt.group(2)) if mt.group(2) else 1
-            if x.lstrip("-").isdigit():
-                align = math.gcd(align, int(x) * k)
-            elif x in self.copies:
+            if x in self.copies:
                 return None
-            elif x in self.lanes:
-                c, A = self.lanes[x]
-                coef += c * k
-                align = math.gcd(align, A * k)
-            else:
-                align = math.gcd(align, k)
-        return coef, abs(align) if align else 1 << 20
+            if x in self.lanes:
+                coef += self.lanes[x][0] * k
+            res = self._radd(res, self._rmul(self.residue(x), k))
+        return (coef,) + res
+
+    def lane_affine(self, expr: str):
+        """(coef, A, c) when ``expr`` (which reads lane vars) is lane-affine with its
+        lane-0 value given by the expression itself; None when the lanes diverge."""
+        return self.affine_info(expr)
 
     def define(self, ctype: str, name: str, expr: str, aff=None) -> None:
         """Emit ``ctype name = expr`` — per lane when expr reads lane vars (unless
@@ -472,6 +549,9 @@ class Fn:
             self.define("const int", v, expr, aff)
         else:
             self._emit(f"const int {v} = {expr};")
+        info = self.affine_info(expr)
+        if info is not None and info[1] != 1:
+            self.al[v] = info[1:]
         self.memo_put(("i", expr), v)
         if uni:
             self.uniform.add(v)
@@ -506,6 +586,7 @@ class Fn:
         # hoisted: emitted into the preamble (before any scope) by the caller
         if d.bstride * MAX_BATCH < 2**31:
             self.pre.append(f"const int {b} = (int)n * {d.bstride};")
+            self.al[b] = (d.bstride, 0)
             r = (self.ptr(d.slot), b)
         else:
             self.pre.append(f"float* __restrict__ {b} = {self.ptr(d.slot)} + n * {d.bstride}LL;")
@@ -601,10 +682,14 @@ class Fn:
         """Vector mode: (address, coef) — lane e reads address + coef*e — or
         (address, None) when the lanes need their own addresses (substituted)."""
         a = self.addr(d, coords)
-        lane, _ = self.offset_parts(d, coords)
+        lane, uni = self.offset_parts(d, coords)
         _, nb = self.base(d)
-        if nb and "n" not in self.uniform and lane != "0":
-            lane = self.ivar(f"{nb} + {lane}")
+        if nb and "n" in self.uniform:
+            uni = nb if uni == "0" else self.ivar(f"{nb} + {uni}")
+        elif nb:
+            lane = nb if lane == "0" else self.ivar(f"{nb} + {lane}")
+        # residue of the lane-0 element offset from the (16 B aligned) slot pointer
+        self._vec_res = self._radd(self.residue(lane), self.residue(uni)) if nb or d.bstride % 4 == 0 else (1, 0)
         if lane in self.lanes:
             return a, self.lanes[lane][0]
         if self.lane_vars(a):
@@ -664,6 +749,14 @@ class Fn:
         return self.fvar(f"__ldg({self.addr(d, coords)})")
 
     def _load_vec(self, d: TDesc, coords, preds) -> str:
+        old_tag = self.cur_tag
+        self.cur_tag = "l"
+        try:
+            return self._load_vec_tagged(d, coords, preds)
+        finally:
+            self.cur_tag = old_tag
+
+    def _load_vec_tagged(self, d: TDesc, coords, preds) -> str:
         a, c = self.vec_addr(d, coords)
         pe = " && ".join(preds)
         key = ("ldv", a, pe)
@@ -672,8 +765,70 @@ class Fn:
             return got
         if c == 0 and not (pe and self.lane_vars(pe)):
             v = self.fvar(f"({pe}) ? __ldg({a}) : 0.f" if pe else f"__ldg({a})")  # lane-invariant
-        else:
+        elif c == 1 and self.V == 4 and VEC16 and (self._vec_res[0] % 4 == 0 or VEC_RT):
+            # unit-stride quad: the aligned 16 B chunk(s) holding it.  Offset m =
+            # (lane-0 offset) mod 4 from a 16 B boundary is static when the residue
+            # analysis knows it (m = 0: one load), else read from the address (row-
+            # dependent shifts).  Lanes 0..3-m sit in the first chunk, 4-m..3 in the
+            # second; a chunk is read only when one of its lanes is valid, so it lies
+            # inside the tensor.  The per-lane select runs on the packed word ``bits``
+            # (4 lane-valid bits | m << 4) — tagged 's', so a load / compute split
+            # leaves only the chunk loads in the load half.
+            static = self._vec_res[0] % 4 == 0
+            m = self._vec_res[1] % 4 if static else None
+            self.nld["aligned" if static and m == 0 else "shifted"] += 1
             v = self.fresh("v")
+            self.vec16 = True
+            pl = [self.subst(pe, e) for e in range(4)] if pe and self.lane_vars(pe) else []
+            zero = "make_float4(0.f, 0.f, 0.f, 0.f)"
+            q = self.fresh("q")
+            self._emit(f"const float* const {q} = {a};")
+            if static:
+                mv = str(m)
+            else:
+                mv = self.fresh("m")
+                self._emit(f"const int {mv} = (int)((reinterpret_cast<unsigned long long>({q}) >> 2) & 3ull);")
+            if static:
+                conds = []
+                for ci in ([0] if m == 0 else [0, 1]):
+                    lanes_ci = [e for e in range(4) if (m + e) // 4 == ci]
+                    conds.append(" || ".join(f"({pl[e]})" for e in lanes_ci) if pl else pe)
+            elif pl:
+                conds = [" || ".join([f"({pl[0]})"] + [f"(({pl[e]}) && {mv} < {4 - e})" for e in (1, 2, 3)]),
+                         f"{mv} > 0 && (" + " || ".join([f"({pl[3]})", f"(({pl[2]}) && {mv} >= 2)", f"(({pl[1]}) && {mv} >= 3)"]) + ")"]
+            else:
+                conds = [pe, f"{mv} > 0" + (f" && ({pe})" if pe else "")]
+            for ci, cond in enumerate(conds):
+                off = f" + {4 * ci - m}" if static and 4 * ci - m else ("" if static else f" - {mv}" + (" + 4" if ci else ""))
+                src = f"__ldg(reinterpret_cast<const float4*>({q}{off}))"
+                self._emit(f"const float4 {v}q{ci} = ({cond}) ? {src} : {zero};" if cond else f"const float4 {v}q{ci} = {src};")
+            bits = None
+            if pl or not static:
+                bits = self.fresh("bits")
+                parts = [f"(({pl[e]}) ? {1 << e} : 0)" for e in range(4)] if pl else ["15"]
+                if not static:
+                    parts.append(f"({mv} << 4)")
+                self._emit(f"const int {bits} = {' | '.join(parts)};")
+            self.cur_tag = "s"
+            w = [f"{v}q0.{x}" for x in "xyzw"] + [f"{v}q1.{x}" for x in "xyzw"]
+            for e in range(4):
+                if static:
+                    sel = w[m + e]
+                else:
+                    mb = f"({bits} >> 4)"
+                    sel = f"({mb} == 0 ? {w[e]} : {mb} == 1 ? {w[e + 1]} : {mb} == 2 ? {w[e + 2]} : {w[e + 3]})"
+                self._emit(f"const float {v}_{e} = ({bits} & {1 << e}) ? {sel} : 0.f;" if pl else f"const float {v}_{e} = {sel};")
+            self.cur_tag = "l"
+            self.copies.add(v)
+        else:
+            self.nld["shifted" if c == 1 else "lanes"] += 1
+            v = self.fresh("v")
+            if c is not None and "(" in a:
+                # one address for the lanes (predicated loads would otherwise each
+                # recompute it under their own predicate)
+                q = self.fresh("q")
+                self._emit(f"const float* const {q} = {a};")
+                a = q
             for e in range(self.V):
                 ae = f"{a} + {c * e}" if c is not None and c * e else (a if c is not None else self.subst(a, e))
                 pl = self.subst(pe, e) if pe else ""
@@ -683,6 +838,25 @@ class Fn:
         return v
 
     def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
+        if self.V > 1:
+            a, c = self.vec_addr(d, coords)
+            if c == 0:
+                raise VecUnsupported("lane-invariant store")
+            if c == 1 and self.V == 4 and VEC16 and self._vec_res[0] % 4 == 0 and self._vec_res[1] % 4 == 0:
+                self.vec16 = True
+                vs = ", ".join(self.subst(val, e) for e in range(4))
+                q = self.fresh("q")
+                self._emit(f"float4* const {q} = reinterpret_cast<float4*>({a});")
+                if beta:
+                    self._emit(f"if (a.beta) {{ const float4 o_ = *{q}; const float4 u_ = make_float4({vs}); *{q} = make_float4(o_.x + u_.x, o_.y + u_.y, o_.z + u_.z, o_.w + u_.w); }} else *{q} = make_float4({vs});")
+                else:
+                    self._emit(f"*{q} = make_float4({vs});")
+                return
+            for e in range(self.V):
+                ae = (f"{a} + {c * e}" if c * e else a) if c is not None else self.subst(a, e)
+                ve = self.subst(val, e)
+                self._emit(f"if (a.beta) *({ae}) += {ve}; else *({ae}) = {ve};" if beta else f"*({ae}) = {ve};")
+            return
         a = self.addr(d, coords)
         if beta:
             self.emit(f"if (a.beta) *({a}) += {val}; else *({a}) = {val};")
@@ -1072,19 +1246,28 @@ class Lowerer:
         self.p.kernel_names.append(name)
         return len(self.p.kernel_names) - 1
 
-    def functor_pointwise(self, name: str, per_image: int, body_fn, planes=None) -> tuple[str, list]:
+    def functor_pointwise(self, name: str, per_image: int, body_fn, planes=None, V: int = 1) -> tuple[str, list]:
         """Functor for ``canvas::pointwise``: one output element (or row) per call;
-        with ``planes`` = (channel ext, spatial ext), for ``canvas::pointwise_planes``."""
+        with ``planes`` = (channel ext, spatial ext), for ``canvas::pointwise_planes``.
+        V = 4: ``run4`` evaluates the 4 consecutive elements r .. r+3 (r a multiple
+        of 4) for ``canvas::pointwise4`` / ``pointwise_planes4`` (raises
+        VecUnsupported when the body cannot be emitted in that form)."""
         f = Fn(self)
         f.pre = []
         f.computing = None
         f.planes = planes
+        if V > 1:
+            f.V = V
+            f.lanes = {"r": (1, V, 0)} if planes is None else {"r": (1, V, 0), "s": (1, V, 0)}
         body_fn(f)
+        self._fn_vec16 = f.vec16
+        self._fn_nld = dict(f.nld)
+        fn = "run4" if V > 1 else "run"
         if planes is None:
-            src = [f"struct {name}_F {{", f"  static constexpr long long PER = {per_image}LL;", "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int r) {"]
+            src = [f"struct {name}_F {{", f"  static constexpr long long PER = {per_image}LL;", f"  static __device__ __forceinline__ void {fn}(const CanvasArgs& a, const long long n, const int r) {{"]
         else:
             Q, S = math.prod(planes[0]), math.prod(planes[1])
-            src = [f"struct {name}_F {{", f"  static constexpr int Q = {Q}, S = {S};", "  static __device__ __forceinline__ void run(const CanvasArgs& a, const long long n, const int q, const int s) {", f"    const int r = q * {S} + s;"]
+            src = [f"struct {name}_F {{", f"  static constexpr int Q = {Q}, S = {S};", f"  static __device__ __forceinline__ void {fn}(const CanvasArgs& a, const long long n, const int q, const int s) {{", f"    const int r = q * {S} + s;"]
         src += ["    " + s for s in f.pre]
         src += f.lines
         src += ["  }", "};"]
@@ -1114,19 +1297,42 @@ class Lowerer:
             # so these keep the flat grid-stride mapping with predicated loads
             planes = None
             functor, slots = self.functor_pointwise(name, per_image, body_fn, None)
+        # 4 consecutive elements per thread (shared index math, one address per
+        # lane-affine gather) when the elements per image / plane divide by 4
+        vec = None
+        if VEC_POINTWISE and (per_image if planes is None else math.prod(planes[1])) % 4 == 0:
+            try:
+                vec = self.functor_pointwise(name, per_image, body_fn, planes, V=4)
+                # gathers mostly at sub-16 B shifts (col2im over a 9C gradient): the
+                # quad form costs occupancy without saving L1 wavefronts (measured
+                # 0.52 vs 0.57 ms on seed-7 #1 layer1 grad n1) — keep one element per thread
+                if self._fn_nld["shifted"] > self._fn_nld["aligned"]:
+                    vec = None
+            except VecUnsupported:
+                vec = None
+        vec16 = False
+        if vec is not None:
+            functor, slots = vec
+            vec16 = self._fn_vec16
         if planes is None:
             v = POINTWISE_VEC
-            launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {v}>(a); }}\n'
             block = POINTWISE_BLOCK
-            grid = (GridRule(per_image, 0, POINTWISE_BLOCK * v, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+            if vec is not None:
+                launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise4<{name}_F>(a); }}\n'
+                grid = (GridRule(per_image, 0, POINTWISE_BLOCK * 4, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+            else:
+                launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise<{name}_F, {v}>(a); }}\n'
+                grid = (GridRule(per_image, 0, POINTWISE_BLOCK * v, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
         else:
             Q, S = math.prod(planes[0]), math.prod(planes[1])
-            chunks = -(-S // POINTWISE_BLOCK)
-            block = -(-(-(-S // chunks)) // 32) * 32
-            launcher = f'extern "C" __global__ void __launch_bounds__({block}) {name}(const CanvasArgs a) {{ canvas::pointwise_planes<{name}_F>(a); }}\n'
+            Sv = S // 4 if vec is not None else S
+            chunks = -(-Sv // POINTWISE_BLOCK)
+            block = -(-(-(-Sv // chunks)) // 32) * 32
+            tmpl = "pointwise_planes4" if vec is not None else "pointwise_planes"
+            launcher = f'extern "C" __global__ void __launch_bounds__({block}) {name}(const CanvasArgs a) {{ canvas::{tmpl}<{name}_F>(a); }}\n'
             grid = (GridRule(0, chunks, 1), GridRule(Q, 0, 1, min(65535, max(1, PLANES_CTAS // chunks))), GridRule(0, 1, 1))
         k = self.add_kernel(name, functor, launcher)
-        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops, align16=vec16))
 
     # ---- forward
     def fwd_targets(self, v: int) -> list:
@@ -1249,6 +1455,8 @@ class Lowerer:
             stmt_fn(c, x)
             f.close()
 
+        if f.V * S > SOFTMAX_REG_SPAN and f.V > 1:
+            raise VecUnsupported("softmax rows of 4 lanes do not fit in registers")
         if S <= SOFTMAX_REG_SPAN:
             # short rows: evaluate the input once into registers (fully unrolled), so
             # the row is read from memory once instead of three times
@@ -1471,21 +1679,94 @@ class Lowerer:
         f.uniform = {uvar}
         f.hoist = True
         f.V = 4
-        f.lanes = {"s": (1, 4)}
+        f.lanes = {"s": (1, 4, 0)}
         try:
             val = fn(f)
         except VecUnsupported:
             return []
+        self._op_vec16 = self._op_vec16 or f.vec16
         mem = [uvar + "_"] + list(f.uni_vars)
         out = [f"  struct {name}R {{ int {', '.join(mem)}; }};"]
         out.append(f"  static __device__ __forceinline__ {name}R {name}row(const CanvasArgs& a, const int {uvar}) {{")
         out += ["    " + ln for ln in f.uni_lines]
         out += [f"    {name}R R;", f"    R.{uvar}_ = {uvar};"] + [f"    R.{v} = {v};" for v in mem[1:]] + ["    return R;", "  }"]
+        unpack = [f"    const int {uvar} = R.{uvar}_; (void){uvar};"] + [f"    const int {v} = R.{v};" for v in mem[1:]]
+        outs = [val + "_" + str(e) if val in f.copies else val for e in range(4)]
         out.append(f"  static __device__ __forceinline__ void {name}k(const CanvasArgs& a, const {name}R& R, const long long n, const int s, float* o) {{")
-        out.append(f"    const int {uvar} = R.{uvar}_; (void){uvar};")
-        out += [f"    const int {v} = R.{v};" for v in mem[1:]]
-        out += ["    " + ln for ln in f.pre] + f.lines
-        out += [f"    o[{e}] = {val + '_' + str(e) if val in f.copies else val};" for e in range(4)]
+        out += unpack + ["    " + ln for ln in f.pre] + f.lines
+        out += [f"    o[{e}] = {outs[e]};" for e in range(4)]
+        out.append("  }")
+        out += self.split_load_compute(name, f, outs, unpack, uvar, mem)
+        return out
+
+    @staticmethod
+    def split_load_compute(name: str, f: Fn, outs: list, unpack: list, uvar: str, mem: list) -> list:
+        """Load / compute split of a 4-pixel operand functor for software-pipelined
+        producers: ``{name}ld(a, R, n, s, raw)`` issues the gathers (index math,
+        predicates, 16 B chunks) into ``{name}NRAW`` raw registers, ``{name}cp(a, R,
+        raw, o)`` evaluates the pointwise chain from them — so the loads of k-block
+        kb+1 are in flight while k-block kb is combined and stored.  ``{name}SPLIT``
+        is false when the float chain reads index values (guards on computed nodes)."""
+        no = [f"  static constexpr bool {name}SPLIT = false;", f"  static constexpr int {name}NRAW = 1;",
+              f"  static __device__ __forceinline__ void {name}ld(const CanvasArgs&, const {name}R&, const long long, const int, float*) {{}}",
+              f"  static __device__ __forceinline__ void {name}cp(const CanvasArgs&, const {name}R&, const float*, float*) {{}}"]
+        if "x" in f.ltags or not VEC_SPLIT:
+            return no
+        tagged = list(zip(f.lines, f.ltags))
+        ints = {"a", "n", "s", uvar, "R"} | set(mem)
+        for ln in f.pre + [x for x, t in tagged if t in "il"]:
+            m = re.match(r"\s*(?:const int|float\* const|const float\* const|float\* __restrict__) (\w+) =", ln)
+            if m:
+                ints.add(m.group(1))
+        # load half outputs: scalar loads and 16 B chunks (floats), bit words (ints)
+        fl, f4, iw = [], [], []
+        for ln, t in tagged:
+            if t != "l":
+                continue
+            m = re.match(r"\s*const (float4|float|int) (\w+) =", ln)
+            if m:
+                {"float": fl, "float4": f4, "int": iw}[m.group(1)].append(m.group(2))
+        comp = [(x, t) for x, t in tagged if t in "sc"]
+        used = set()
+        for ln, t in comp:
+            m = re.match(r"\s*const float (\w+) = (.*);$", ln)
+            if not m:
+                return no
+            toks = set(_IDENT.findall(m.group(2)))
+            bad = toks & ints - set(iw) if t == "s" else toks & ints
+            if bad:
+                return no
+            used |= toks
+        for o in outs:
+            used |= set(_IDENT.findall(o))
+        fl = [v for v in fl if v in used]
+        f4 = [v for v in f4 if v in used]
+        iw = [v for v in iw if v in used]
+        nr = len(fl) + 4 * len(f4) + len(iw)
+        if not nr:
+            return no
+        out = [f"  static constexpr bool {name}SPLIT = true;", f"  static constexpr int {name}NRAW = {nr};"]
+        out.append(f"  static __device__ __forceinline__ void {name}ld(const CanvasArgs& a, const {name}R& R, const long long n, const int s, float* raw) {{")
+        out += unpack + ["    " + ln for ln in f.pre]
+        out += [x for x, t in tagged if t in "il"]
+        j = 0
+        put, get = [], []
+        for v in fl:
+            put.append(f"    raw[{j}] = {v};")
+            get.append(f"    const float {v} = raw[{j}];")
+            j += 1
+        for v in f4:
+            put.append(f"    raw[{j}] = {v}.x; raw[{j + 1}] = {v}.y; raw[{j + 2}] = {v}.z; raw[{j + 3}] = {v}.w;")
+            get.append(f"    const float4 {v} = make_float4(raw[{j}], raw[{j + 1}], raw[{j + 2}], raw[{j + 3}]);")
+            j += 4
+        for v in iw:
+            put.append(f"    raw[{j}] = __int_as_float({v});")
+            get.append(f"    const int {v} = __float_as_int(raw[{j}]);")
+            j += 1
+        out += put + ["  }"]
+        out.append(f"  static __device__ __forceinline__ void {name}cp(const CanvasArgs& a, const {name}R& R, const float* raw, float* o) {{")
+        out += get + [x for x, _ in comp]
+        out += [f"    o[{e}] = {outs[e]};" for e in range(4)]
         out.append("  }")
         return out
 
@@ -1541,8 +1822,10 @@ class Lowerer:
             "  }",
         ]
         lines += self.split_operand("B", fb, bval, "k")
+        self._op_vec16 = False
         vec = self.vec_operand("B4", bfn, "k", S, fa.local_slots)
         lines += vec + [f"  static constexpr bool VEC = {'true' if vec else 'false'};"]
+        lines += [f"  static constexpr bool SPLIT = {'true' if vec and 'B4SPLIT = true' in chr(10).join(vec) else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
         tc = self.use_tc and M >= 8 and K >= 16
@@ -1595,10 +1878,13 @@ class Lowerer:
                 total = nct * kb * nt * 32
                 self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
                 grid = (GridRule(S * nct, 0, 128, SMS), GridRule(0, 1, 1), GridRule(0, 1, 1))
-                self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=psmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+                self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=psmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vec) and self._op_vec16))
                 return False
             # 2 CTAs x 8 producer warps when a 2-stage ring pairs on an SM, else 1 CTA x 16 warps
             pw = TC_PIX_PW if TC_PIX_PW else (8 if smem <= TC_SMEM_PAIR else 16)
+            mraw = re.search(r"B4NRAW = (\d+)", functor)
+            if not TC_PIX_PW and mraw and "SPLIT = true" in functor and (32 // 8) * int(mraw.group(1)) * 2 > 64:
+                pw = 16  # pipelined producers: two k-blocks of raw gathers per thread must fit in registers
             threads = (pw + 2) * 32
             if pw > 8:
                 stages = max(2, min(4, (220 * 1024) // (2 * 128 * 128 + 2 * nt * 128)))
@@ -1610,7 +1896,7 @@ class Lowerer:
             total = nct * kb * nt * 32
             self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
             grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
-            self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+            self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vec) and self._op_vec16))
             return do_save
         launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_nk<{name}_F>(a); }}\n'
         k = self.add_kernel(name, functor, launcher)
@@ -1651,10 +1937,13 @@ class Lowerer:
         ]
         lines += self.split_operand("A", fa, aval, "m")
         lines += self.split_operand("B", fb, bval, "k")
+        self._op_vec16 = False
         va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots)
         vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots) if va4 else []
         lines += (va4 + vb4) if vb4 else []
         lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'};"]
+        both = vb4 and "A4SPLIT = true" in chr(10).join(va4) and "B4SPLIT = true" in chr(10).join(vb4)
+        lines += [f"  static constexpr bool SPLIT = {'true' if both else 'false'};"]
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
         lines += self.prefetch_members(fa, [fb, fa], S)
         lines += ["};"]
@@ -1673,7 +1962,7 @@ class Lowerer:
             launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}, {pw}, {jg}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
             grid = (GridRule(0, J, 128 * jg), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
-            self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
+            self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vb4) and self._op_vec16))
         elif small:
             jt = min(1 << max(0, (256 // M).bit_length() - 1), WGRAD_SMALL_JT_MAX)
             jt = min(jt, 1 << (J - 1).bit_length()) if J > 1 else 1

@@ -21,6 +21,20 @@ using std::max;
 using std::min;
 template <class T>
 inline T __ldg(const T* p) { return *p; }
+inline float __int_as_float(int i) {
+  float f;
+  std::memcpy(&f, &i, 4);
+  return f;
+}
+inline int __float_as_int(float f) {
+  int i;
+  std::memcpy(&i, &f, 4);
+  return i;
+}
+struct float4 {
+  float x, y, z, w;
+};
+inline float4 make_float4(float x, float y, float z, float w) { return float4{x, y, z, w}; }
 
 #define CANVAS_MAX_KSLOTS 24
 struct CanvasArgs {
@@ -43,6 +57,19 @@ void pointwise_planes(const CanvasArgs& a) {
   for (long long n = 0; n < a.n; ++n)
     for (int q = 0; q < F::Q; ++q)
       for (int s = 0; s < F::S; ++s) F::run(a, n, q, s);
+}
+
+template <class F>
+void pointwise4(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int r = 0; r < (int)F::PER; r += 4) F::run4(a, n, r);
+}
+
+template <class F>
+void pointwise_planes4(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int q = 0; q < F::Q; ++q)
+      for (int s = 0; s < F::S; s += 4) F::run4(a, n, q, s);
 }
 
 template <class F>
