@@ -608,6 +608,16 @@ __device__ __forceinline__ void tmem_ld16(cv_u32 taddr, float* v) {
   for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+__device__ __forceinline__ void tmem_ld8(cv_u32 taddr, float* v) {
+  cv_u32 r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 __device__ __forceinline__ void tmem_ld32(cv_u32 taddr, float* v) {
   cv_u32 r[32];
   asm volatile(
@@ -1079,7 +1089,7 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], EW * 32);
+      mbar_init(&tempty[i], (F::EPI_BC ? 4 : EW) * 32);  // EPI_BC: one warpgroup drains a tile
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1268,6 +1278,50 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
     // with EW = 8 the two warpgroups split the columns
     const int q = warp & 3;
     const int part = (warp - PW - 2) >> 2;  // 0 .. EW/4-1
+    if constexpr (F::EPI_BC) {
+      // broadcast-adjoint epilogue: TMEM columns of a tile are m*JT + jj (replica m
+      // of lhs index j0 + jj), so the thread owning a pixel row writes the rhs
+      // contribution of every column and sums the lhs terms over the replicas in
+      // registers.  Warpgroups take alternate tiles (= alternate TMEM buffers).
+      constexpr int JT = F::EPI_JT, MR = F::EPI_M, NWG = EW / 4;
+      static_assert(JT == 8 || JT == 16, "column group of 8 or 16");
+      int it = 0;
+      for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x, ++it) {
+        if (it % NWG != part) continue;
+        const int buf = it & 1;
+        const long long t0 = (tile / NCT) * kBM;
+        const int j0 = (int)(tile % NCT) * JT;
+        const long long te = t0 + q * 32 + lane;
+        const bool eok = te < T;
+        const long long en = eok ? te / F::S : 0;
+        const int es = eok ? (int)(te - en * F::S) : 0;
+        float lv[JT], dl[JT];
+#pragma unroll
+        for (int jj = 0; jj < JT; ++jj) {
+          lv[jj] = eok ? F::epi_lhs(a, en, j0 + jj, es) : 0.f;
+          dl[jj] = 0.f;
+        }
+        mbar_wait(&tfull[buf], (cv_u32)((it >> 1) & 1));
+        fence_after();
+#pragma unroll 1
+        for (int m = 0; m < MR; ++m) {
+          float g[JT];
+          const cv_u32 ta = tmem + buf * NT + ((cv_u32)(q * 32) << 16) + m * JT;
+          if constexpr (JT == 16) tmem_ld16(ta, g);
+          else tmem_ld8(ta, g);
+          if (eok) {
+#pragma unroll
+            for (int jj = 0; jj < JT; ++jj) dl[jj] += F::epi_term(a, en, m, j0 + jj, es, g[jj], lv[jj]);
+          }
+        }
+        fence_before();
+        mbar_arrive(&tempty[buf]);
+        if (eok) {
+#pragma unroll
+          for (int jj = 0; jj < JT; ++jj) F::epi_store_l(a, en, j0 + jj, es, dl[jj]);
+        }
+      }
+    } else {
     constexpr int CPART = ((NT / (EW / 4)) + 31) / 32 * 32;
     int it = 0;
     for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x, ++it) {
@@ -1295,6 +1349,7 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
       }
       fence_before();
       mbar_arrive(&tempty[buf]);
+    }
     }
   }
   fence_before();

@@ -129,9 +129,11 @@ def _run_once(dp, plan, x, ws, dy, device):
     return y.cpu(), dx.cpu(), [d.cpu() for d in dws]
 
 
-def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5, prepared: dict | None = None, parity_batch: int = 0, checker=None) -> dict:
-    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events);
-    with ``parity_batch`` and ``checker``: the parity sample (module doc, step 4)."""
+def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, iters: int = 5, prepared: dict | None = None, parity_batch: int = 0, checker=None, graph: bool = True) -> dict:
+    """Plan + fwd/bwd latency of one kernel on ``cuda:device`` (CUDA events; with
+    ``graph`` replayed from one CUDA graph per direction, eager timings in
+    ``extra``); with ``parity_batch`` and ``checker``: the parity sample (module
+    doc, step 4)."""
     import torch
 
     sh = dict(CONFIG1, **(shapes or {}))
@@ -155,17 +157,44 @@ def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, it
     for _ in range(2):
         dp.forward(x, ws, y, saved, st)
         dp.backward(x, ws, saved, dy, dx, dws, work, st)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    ev[0].record()
-    for _ in range(iters):
-        dp.forward(x, ws, y, saved, st)
-    ev[1].record()
-    for _ in range(iters):
-        dp.backward(x, ws, saved, dy, dx, dws, work, st)
-    ev[2].record()
-    torch.cuda.synchronize(dev)
+
+    def timed(fwd, bwd):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev[0].record()
+        for _ in range(iters):
+            fwd()
+        ev[1].record()
+        for _ in range(iters):
+            bwd()
+        ev[2].record()
+        torch.cuda.synchronize(dev)
+        return ev[0].elapsed_time(ev[1]) / iters, ev[1].elapsed_time(ev[2]) / iters
+
+    fwd_e, bwd_e = timed(lambda: dp.forward(x, ws, y, saved, st), lambda: dp.backward(x, ws, saved, dy, dx, dws, work, st))
+    extra = {"launches_fwd": dp.launches(0), "launches_bwd": dp.launches(1), "fwd_ms_eager": fwd_e, "bwd_ms_eager": bwd_e}
+    fwd_ms, bwd_ms = fwd_e, bwd_e
+    if graph:
+        # one CUDA graph per (plan, batch) for each direction: a config-1 kernel is
+        # 4-16 short launches, so the eager numbers are host-launch bound; the
+        # graph replay is the device latency the search ranks candidates by
+        try:
+            gf, gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream(dev)
+            cs.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(gf, stream=cs):
+                    dp.forward(x, ws, y, saved, cs.cuda_stream)
+                with torch.cuda.graph(gb, stream=cs):
+                    dp.backward(x, ws, saved, dy, dx, dws, work, cs.cuda_stream)
+            torch.cuda.current_stream(dev).wait_stream(cs)
+            gf.replay()
+            gb.replay()
+            fwd_ms, bwd_ms = timed(gf.replay, gb.replay)
+            extra["graph"] = True
+        except Exception as e:  # capture unsupported here: eager timings stand
+            extra["graph"] = False
+            extra["graph_error"] = str(e)[:200]
     finite = bool(torch.isfinite(y).all()) and bool(torch.isfinite(dx).all())
-    extra = {"launches_fwd": dp.launches(0), "launches_bwd": dp.launches(1)}
     status = "ok" if finite else "nonfinite"
     if parity_batch > 0 and checker is not None:
         px, pws, pdy = parity_inputs(plan, sh, parity_batch)
@@ -177,8 +206,8 @@ def evaluate_kernel(ir_text: str, device: int, *, shapes: dict | None = None, it
     return {
         "status": status,
         "plan_ms": plan_ms,
-        "fwd_ms": ev[0].elapsed_time(ev[1]) / iters,
-        "bwd_ms": ev[1].elapsed_time(ev[2]) / iters,
+        "fwd_ms": fwd_ms,
+        "bwd_ms": bwd_ms,
         "fc_macs_per_image": plan.graph.fc_macs_per_image(),
         "extra": extra,
     }

@@ -76,6 +76,7 @@ VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launche
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = os.environ.get("CANVAS_VEC_RT", "0") == "1"  # quads at a run-time 4 B offset: two 16 B loads + select (measured 1.7x slower on the layer1 GEMMs: off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
+EPI_BC = os.environ.get("CANVAS_EPI_BC", "1") == "1"  # FC dgrad epilogue applies the input broadcast's adjoint
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
 TC_WGRAD_JG_MAX = int(os.environ.get("CANVAS_WGRAD_JG", "1"))  # max row tiles per wgrad CTA (1 vs 2: +0.5% img/s on config 2 with 8192-pixel chunks)
@@ -913,6 +914,12 @@ class Lowerer:
         self.inline_dgrad: set = set()  # few-output FCs whose input-gradient contribution is evaluated inline
         self.dot_desc: dict[int, TDesc] = {}  # softmax node u -> row dot buffer
         self.computing_grad = None
+        # FC dgrads whose epilogue applies the adjoint of their input broadcast
+        # (u -> jt): the epilogue writes the broadcast's edge contributions
+        # (edge_desc[(bcast, pos)]) and gradients that need no other term (grad_by_epi)
+        self.epi_bc: dict = {}
+        self.edge_desc: dict = {}
+        self.grad_by_epi: set = set()
 
     @classmethod
     def bare(cls, plan: Plan, use_tc: bool = True) -> "Lowerer":
@@ -925,6 +932,7 @@ class Lowerer:
         lw.fwd_desc, lw.count_desc, lw.grad_desc, lw.dgrad_desc, lw.dot_desc = {}, {}, {}, {}, {}
         lw.inline_dgrad = set()
         lw.computing_grad = None
+        lw.epi_bc, lw.edge_desc, lw.grad_by_epi = {}, {}, set()
         return lw
 
     # -------------------------------------------------------------- materialisation
@@ -1191,6 +1199,8 @@ class Lowerer:
     def bcast_contrib(self, f: Fn, nu, pos: int, v: int, coords: tuple) -> str:
         at = nu.attr
         u = nu.id
+        if (u, pos) in self.edge_desc:  # written by the epilogue of the consuming FC's dgrad
+            return f.load(self.edge_desc[(u, pos)], coords)
         lhs_n, rhs_n = nu.ins
         bop = at["op"]
         total = []
@@ -1797,10 +1807,12 @@ class Lowerer:
         body.append("  }")
         return [f"  static constexpr int NPF = {sum(r for _, _, r in rows)};"] + body
 
-    def emit_gemm_nk(self, name, fa: Fn, a_expr: str, bfn, sfn, M, K, S, phase, beta, what, nbytes, flops, save=None) -> bool:
+    def emit_gemm_nk(self, name, fa: Fn, a_expr: str, bfn, sfn, M, K, S, phase, beta, what, nbytes, flops, save=None, epi=None) -> bool:
         """C[n][m][s] = sum_k A(m,k) * B(n,k,s) through canvas::gemm_nk (one shared slot table).
         ``save(f)``: emit the store of B's value ``val`` at (n, k, s) — the operand
-        write-back; honoured (returns True) only on the non-persistent tcgen05 path."""
+        write-back; honoured (returns True) only on the non-persistent tcgen05 path.
+        ``epi`` = (NT, functor lines): a custom TMEM epilogue (EPI_BC) on the
+        persistent tcgen05 path with column tiles of NT."""
         fb = Fn(self)
         fb.pre = []
         fb.computing = None
@@ -1813,7 +1825,8 @@ class Lowerer:
         fs.computing = None
         fs.local_slots = fa.local_slots
         fs.uniform = {"m"}  # TMEM epilogue: column per iteration, lane = pixel
-        sfn(fs, "acc")
+        if sfn is not None:
+            sfn(fs, "acc")
         lines = [
             f"struct {name}_F {{",
             f"  static constexpr int M = {M}, K = {K}, S = {S};",
@@ -1828,7 +1841,10 @@ class Lowerer:
         lines += [f"  static constexpr bool SPLIT = {'true' if vec and 'B4SPLIT = true' in chr(10).join(vec) else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
+        lines += epi[1] if epi else ["  static constexpr bool EPI_BC = false;", "  static constexpr int EPI_M = 1, EPI_JT = 16;"]
         tc = self.use_tc and M >= 8 and K >= 16
+        if epi and not tc:
+            raise LoweringError("epilogue fusion needs the tensor-core dgrad")
         nacc0 = 1
         while nacc0 < 4 and K > TC_ACC_K * nacc0:
             nacc0 *= 2
@@ -1855,6 +1871,8 @@ class Lowerer:
             while nacc < 4 and K > TC_ACC_K * nacc:
                 nacc *= 2
             nt, nct, stages = tc_tile(M, min(TC_NTMAX, 512 // nacc))
+            if epi:
+                nt, nct = epi[0], M // epi[0]
             smem = tc_smem_bytes(nt, stages)
             kb = -(-K // 32)
             pack_bytes = nct * kb * 2 * nt * 128
@@ -1867,7 +1885,7 @@ class Lowerer:
                 pslot = -1 - k_ws
             ploc = fa.ptr(pslot)
             functor = functor[: functor.rindex("};")] + f"  static __device__ __forceinline__ float* packed(const CanvasArgs& a) {{ return {ploc}; }}\n}};\n"
-            if TC_PERSIST and K < 4 * nt:  # epilogue-heavy: overlap stores with the next tile
+            if epi or (TC_PERSIST and K < 4 * nt):  # epilogue-heavy: overlap stores with the next tile
                 pstages, psmem = tc_persist_cfg(nt)
                 pw = TC_PW if K > 128 else 4  # short reductions: cheap mainloop, store-bound epilogue
                 ew = 8 if nt >= 128 else 4
@@ -1994,6 +2012,11 @@ class Lowerer:
         dx_beta = BETA_ALWAYS if stride_gt1 else (BETA_AFTER_FIRST if (p.copies > 1 and p.mode == "concat") else BETA_NONE)
         if stride_gt1:
             p.launches.append(Launch("memset", 1, "dx_zero", memset_slot=SLOT_DX, memset_size=SizeRule(4 * p.c_in * p.h_in * p.w_in, 1, 0), what="dx zero-fill (stride > 1)"))
+        # FC dgrads that absorb the adjoint of their input broadcast (epilogue fusion)
+        for u in (nd.id for nd in self.nodes if nd.op == "fc"):
+            jt = self.epi_bc_tile(u)
+            if jt:
+                self.epi_bc[u] = jt
         # where each materialised gradient lives
         for v in sorted(self.grad_mat):
             nd = self.nodes[v]
@@ -2008,6 +2031,19 @@ class Lowerer:
         for u in sorted(self.nodes[i].id for i in range(len(self.nodes)) if self.nodes[i].op == "fc"):
             v = self.nodes[u].ins[0]
             nv = self.nodes[v]
+            if u in self.epi_bc:
+                # dL/dv itself is never stored: the epilogue writes the rhs edge
+                # contribution (shape of v) and the lhs replica sum
+                lhs, rhs = nv.ins
+                _, self.edge_desc[(v, 1)] = self._new_ws(nv.ext)
+                nl = self.nodes[lhs]
+                if lhs in self.grad_mat and len(nl.consumers) == 1:
+                    self.edge_desc[(v, 0)] = self.grad_desc[lhs]
+                    self.grad_by_epi.add(lhs)
+                else:
+                    _, self.edge_desc[(v, 0)] = self._new_ws(nl.ext)
+                self.grad_by_epi.add(v)
+                continue
             if v in self.grad_mat and len(nv.consumers) == 1:
                 if v == 0:
                     self.dgrad_desc[u] = self.dx_desc()
@@ -2027,7 +2063,7 @@ class Lowerer:
         for u in range(len(self.nodes) - 1, -1, -1):
             nu = self.nodes[u]
             # 1) materialise dL/du if it is a gradient sum point (not dy, not aliased to an FC dgrad)
-            if u in self.grad_mat and not self._grad_is_fc_alias(u):
+            if u in self.grad_mat and not self._grad_is_fc_alias(u) and u not in self.grad_by_epi:
                 beta = dx_beta if u == 0 else BETA_NONE
                 d = self.grad_desc[u]
                 name = f"k{len(p.kernel_names)}_bwd_grad{u}"
@@ -2103,6 +2139,10 @@ class Lowerer:
         if u in self.inline_dgrad:
             self.lower_fc_wgrad(u)
             return
+        if u in self.epi_bc:
+            self.lower_fc_dgrad_bc(u)
+            self.lower_fc_wgrad(u)
+            return
         dd = self.dgrad_desc[u]
         beta = dx_beta if dd.slot == SLOT_DX else BETA_NONE
         flops = 2 * O * K * S
@@ -2140,6 +2180,106 @@ class Lowerer:
 
             self.emit_gemm_nk(name, fa, a_expr, bfn, sfn, M=K, K=O, S=S, phase=1, beta=beta, what=f"dgrad {K}x{O}x{S} n{u}->n{v}", nbytes=4 * (nu.numel + nv.numel), flops=flops)
         self.lower_fc_wgrad(u)
+
+    def epi_bc_tile(self, u: int):
+        """JT (lhs indices per column tile) when FC u's dgrad can apply the adjoint of
+        its input broadcast v = bcast(op)(lhs, rhs) in its TMEM epilogue, else None.
+        Needs: v read only by u (dL/dv is exactly the dgrad), a tensor-core dgrad,
+        the broadcast core spanning all of v's channel dims (no prefix), and a column
+        tile of M replicas x JT lhs indices that fits one MMA (N = M*JT <= 256)."""
+        if not EPI_BC or not self.use_tc:
+            return None
+        nu = self.nodes[u]
+        v = nu.ins[0]
+        nv = self.nodes[v]
+        if v == 0 or nv.op != "bcast" or len(nv.consumers) != 1 or 0 in nv.ins:
+            return None
+        O, K = self.g.fc_shape(u)
+        if min(O, K) <= SMALL_FC or O < 16 or K < 8:
+            return None
+        at = nv.attr
+        if at["cs"] != 0 or at["nr"] != nv.nch or at["M"] < 2:
+            return None
+        L, M = at["L"], at["M"]
+        for jt in (16, 8):
+            if L % jt == 0 and (M * jt) % 16 == 0 and M * jt <= 256:
+                return jt
+        return None
+
+    def lower_fc_dgrad_bc(self, u: int) -> None:
+        """dgrad of FC u (tcgen05, persistent) with the input broadcast's adjoint in
+        the epilogue.  Columns of dL/dv are packed replica-major per tile — tile ct
+        holds k = m*L + ct*JT + jj (m < M, jj < JT) — so each epilogue thread (one
+        pixel) owns all M replicas of its JT lhs indices: it writes the rhs edge
+        contribution dv * d op/d rhs per column and sums dv * d op/d lhs over the
+        replicas in registers (App. A.8 tie split, replica order m = 0..M-1).
+        Removes the materialised 9C gradient and the replica-sum pass (SURVEY §7,
+        PAPER.md:177: an Unfold never copies)."""
+        nu = self.nodes[u]
+        v = nu.ins[0]
+        nv = self.nodes[v]
+        lhs_n, rhs_n = nv.ins
+        at = nv.attr
+        L, M, op = at["L"], at["M"], at["op"]
+        jt = self.epi_bc[u]
+        nt = M * jt
+        O, K = self.g.fc_shape(u)
+        S = math.prod(nu.sp_ext)
+        wslot, _ = self.fc_weight_slot(u)
+        flops = 2 * O * K * S
+        name = f"k{len(self.p.kernel_names)}_bwd_dgrad{u}"
+        fa = Fn(self)
+        fa.pre = []
+        fa.computing = None
+        # packed column col of tile ct = col / NT -> k = m*L + ct*JT + jj
+        a_expr = f"__ldg({fa.ptr(wslot)} + k*{K} + ((m % {nt}) / {jt}) * {L} + (m / {nt}) * {jt} + (m % {jt}))"
+
+        def bfn(f):
+            sp = tuple(f.decompose("s", nu.sp_ext))
+            return self.grad(f, u, ("k",) + sp)
+
+        need_r = op in ("min", "max", "mul")
+        need_l = op in ("min", "max", "mul")
+        ld, rd = self.edge_desc[(v, 0)], self.edge_desc[(v, 1)]
+
+        def mk(sig, body, uni):
+            f = Fn(self)
+            f.pre = []
+            f.computing = None
+            f.local_slots = fa.local_slots
+            f.uniform = set(uni)
+            ret = body(f)
+            out = [f"  static __device__ __forceinline__ {sig} {{"] + ["    " + x for x in f.pre] + f.lines
+            if ret is not None:
+                out.append(f"    return {ret};")
+            return out + ["  }"]
+
+        def lhs_val(f):
+            lc = tuple(f.decompose("j", at["lcore"]))
+            sp = tuple(f.decompose("s", nv.sp_ext))
+            return self.val(f, lhs_n, lc + sp) if need_l else "0.f"
+
+        def term(f):
+            kk = f.ivar(f"m*{L} + j")
+            rc = tuple(f.decompose(kk, at["rcore"]))
+            sp = tuple(f.decompose("s", nv.sp_ext))
+            r = self.val(f, rhs_n, rc + sp) if need_r else "0.f"
+            dr = f.fvar(_bc_d_rhs(op, "g", "l", r))
+            f.store(rd, rc + sp, dr, False)
+            return f.fvar(_bc_d_lhs(op, "g", "l", r))
+
+        def store_l(f):
+            lc = tuple(f.decompose("j", at["lcore"]))
+            sp = tuple(f.decompose("s", nv.sp_ext))
+            f.store(ld, lc + sp, "dl", False)
+
+        epi = [f"  static constexpr bool EPI_BC = true;", f"  static constexpr int EPI_M = {M}, EPI_JT = {jt};"]
+        epi += mk("float epi_lhs(const CanvasArgs& a, const long long n, const int j, const int s)", lhs_val, {"j"})
+        epi += mk("float epi_term(const CanvasArgs& a, const long long n, const int m, const int j, const int s, const float g, const float l)", term, {"m", "j"})
+        epi += mk("void epi_store_l(const CanvasArgs& a, const long long n, const int j, const int s, const float dl)", store_l, {"j"})
+        self.emit_gemm_nk(name, fa, a_expr, bfn, None, M=K, K=O, S=S, phase=1, beta=BETA_NONE,
+                          what=f"dgrad+bcast adjoint {K}x{O}x{S} n{u}->n{lhs_n},n{v}",
+                          nbytes=4 * (nu.numel + nv.numel + self.nodes[lhs_n].numel), flops=flops, epi=(nt, epi))
 
     def lower_fc_wgrad(self, u: int) -> None:
         """dW[o,i] = sum_{n,s} dL/du[n,o,s] * v[n,i,s]."""

@@ -198,9 +198,39 @@ void gemm_wgrad_vec(const CanvasArgs& a) {
   delete[] bv;
 }
 
+// dgrad with the broadcast-adjoint epilogue (F::EPI_BC): packed column
+// col = ct*NT + m*JT + jj holds replica m of lhs index j = ct*JT + jj
+template <class F>
+void gemm_nk_epi_bc(const CanvasArgs& a) {
+  const long long T = a.n * (long long)F::S;
+  constexpr int NT = F::EPI_M * F::EPI_JT, L = F::M / F::EPI_M;
+  float* col = new float[F::K];
+  float* out = new float[F::M];
+  for (long long t = 0; t < T; ++t) {
+    const long long n = t / F::S;
+    const int s = (int)(t - n * F::S);
+    for (int k = 0; k < F::K; ++k) col[k] = F::B(a, n, k, s);
+    for (int m = 0; m < F::M; ++m) {
+      float acc = 0.f;
+      for (int k = 0; k < F::K; ++k) acc = std::fma(F::A(a, m, k), col[k], acc);
+      out[m] = acc;
+    }
+    for (int j = 0; j < L; ++j) {
+      const float l = F::epi_lhs(a, n, j, s);
+      float dl = 0.f;
+      for (int m = 0; m < F::EPI_M; ++m)
+        dl += F::epi_term(a, n, m, j, s, out[(j / F::EPI_JT) * NT + m * F::EPI_JT + j % F::EPI_JT], l);
+      F::epi_store_l(a, n, j, s, dl);
+    }
+  }
+  delete[] col;
+  delete[] out;
+}
+
 template <class F>
 void gemm_nk_tc(const CanvasArgs& a) {
-  if constexpr (F::VEC) gemm_nk_vec<F>(a);
+  if constexpr (F::EPI_BC) gemm_nk_epi_bc<F>(a);
+  else if constexpr (F::VEC) gemm_nk_vec<F>(a);
   else gemm_nk<F>(a);
 }
 template <class F>

@@ -43,6 +43,42 @@ def test_vector_producers(name, h, w):
     assert_close(case, *emu_run(case), f"{name} vec {h}x{w}")
 
 
+@pytest.mark.parametrize("cin,cout,stride", [(32, 32, 1), (32, 64, 2), (64, 32, 1)])
+def test_dgrad_bcast_epilogue(cin, cout, stride):
+    """seed-7 #1's K = 9C FC reads bcast(min)(n7, unfold(softmax)): its dgrad epilogue
+    writes the rhs edge contribution and the replica-summed lhs gradient (no
+    materialised 9C gradient, no replica-sum launch)."""
+    case = reference(zoo.SEED7_K1, cin, cout, 6, 8, stride=stride, n=2)
+    assert "EPI_BC = true" in case.plan.source
+    assert not any(L.what == "grad n7" for L in case.plan.launches)
+    assert_close(case, *emu_run(case), f"epi-bc {cin}->{cout} s{stride}")
+
+
+def _epi_sweep(i):
+    import torch
+
+    torch.set_num_threads(1)
+    texts = ["canvas-ir v1\n" + t for t in open("tests/golden/sampler_10_7_256.cir").read().split("canvas-ir v1\n")[1:]]
+    case = reference(texts[i], 32, 32, 4, 4)
+    if "EPI_BC = true" not in case.plan.source:
+        return None, False
+    try:
+        assert_close(case, *emu_run(case), f"sweep #{i} (epi-bc)")
+    except AssertionError as e:
+        return str(e), True
+    return None, True
+
+
+def test_dgrad_bcast_epilogue_sweep():
+    """Every kernel of the first 96 of the 256-kernel sweep whose FC reads a
+    broadcast (at C = 32, where its dgrad is a tensor-core GEMM)."""
+    with ProcessPoolExecutor(min(8, os.cpu_count() or 1), mp_context=multiprocessing.get_context("spawn")) as ex:
+        res = list(ex.map(_epi_sweep, range(96)))
+    errs = [e for e, _ in res if e]
+    assert not errs, errs[:5]
+    assert sum(used for _, used in res) >= 3
+
+
 @pytest.mark.parametrize("cin,cout,stride", [(8, 16, 2), (16, 8, 1), (8, 32, 2)])
 @pytest.mark.parametrize("name", ["seed7_k1", "involution", "seed7_k0"])
 def test_replication(name, cin, cout, stride):
