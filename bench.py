@@ -276,7 +276,7 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--batch", type=int, default=256)
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch (default: the workload's, SURVEY §8d: 512 for config 3, else 256)")
     ap.add_argument("--kernel", default="seed7_k1", choices=sorted(zoo.ALL))
     ap.add_argument("--model", default="resnet18", help="workload backbone (backbones.SPECS): resnet18 = config 2 (default), resnet29 / resnext29_2x64d = config 3, mobilenet_v2 / efficientnet_b0 / vgg16 = config 5")
     ap.add_argument("--impl", default="canvas", choices=["canvas", "reference"])
@@ -287,6 +287,10 @@ def main() -> None:
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly instead of replaying one captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "canvas" else args.warmup
+    if args.batch <= 0:
+        from paper_2304_07741_b200.backbones import SPECS
+
+        args.batch = SPECS[args.model].get("batch", 256)
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_distributed(args.gpus)

@@ -23,8 +23,8 @@ from .module import conv_is_target, replace
 
 SPECS = {
     "resnet18": {"input": (3, 224, 224), "classes": 1000, "kernel_sizes": (3,), "config": 2},
-    "resnet29": {"input": (3, 32, 32), "classes": 10, "kernel_sizes": (1, 3), "config": 3},
-    "resnext29_2x64d": {"input": (3, 32, 32), "classes": 10, "kernel_sizes": (1, 3), "config": 3},
+    "resnet29": {"input": (3, 32, 32), "classes": 10, "kernel_sizes": (1, 3), "config": 3, "batch": 512},
+    "resnext29_2x64d": {"input": (3, 32, 32), "classes": 10, "kernel_sizes": (1, 3), "config": 3, "batch": 512},
     "mobilenet_v2": {"input": (3, 224, 224), "classes": 1000, "kernel_sizes": (1, 3), "config": 5},
     "efficientnet_b0": {"input": (3, 224, 224), "classes": 1000, "kernel_sizes": (1, 3, 5), "config": 5},
     "vgg16": {"input": (3, 224, 224), "classes": 1000, "kernel_sizes": (3,), "config": 5},

@@ -1295,31 +1295,54 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
         const bool eok = te < T;
         const long long en = eok ? te / F::S : 0;
         const int es = eok ? (int)(te - en * F::S) : 0;
-        float lv[JT], dl[JT];
+        // operand values do not depend on the GEMM: the lhs row and replica 0's rhs
+        // gathers are issued before the accumulator is waited on, replica m+1's
+        // while replica m is combined (two register sets, loop unrolled by 2).
+        // Rows past the batch read a clamped pixel and only their stores are
+        // predicated off, so the body stays branch-free.
+        float lv[JT], dl[JT], r0[JT], r1[JT];
 #pragma unroll
         for (int jj = 0; jj < JT; ++jj) {
-          lv[jj] = eok ? F::epi_lhs(a, en, j0 + jj, es) : 0.f;
+          lv[jj] = F::epi_lhs(a, en, j0 + jj, es);
+          r0[jj] = F::epi_rhs(a, en, 0, j0 + jj, es);
           dl[jj] = 0.f;
         }
         mbar_wait(&tfull[buf], (cv_u32)((it >> 1) & 1));
         fence_after();
-#pragma unroll 1
-        for (int m = 0; m < MR; ++m) {
+        // ok: store predicate — the constant true on full tiles (no per-element branch)
+        auto step = [&](int m, float (&rc)[JT], float (&rn)[JT], const bool ok) {
+          if constexpr (F::EPI_PF) {
+            const int mn = m + 1 < MR ? m + 1 : m;
+#pragma unroll
+            for (int jj = 0; jj < JT; ++jj) rn[jj] = F::epi_rhs(a, en, mn, j0 + jj, es);
+          } else if (m > 0) {
+#pragma unroll
+            for (int jj = 0; jj < JT; ++jj) rc[jj] = F::epi_rhs(a, en, m, j0 + jj, es);
+          }
           float g[JT];
           const cv_u32 ta = tmem + buf * NT + ((cv_u32)(q * 32) << 16) + m * JT;
           if constexpr (JT == 16) tmem_ld16(ta, g);
           else tmem_ld8(ta, g);
-          if (eok) {
 #pragma unroll
-            for (int jj = 0; jj < JT; ++jj) dl[jj] += F::epi_term(a, en, m, j0 + jj, es, g[jj], lv[jj]);
+          for (int jj = 0; jj < JT; ++jj) dl[jj] += F::epi_term(a, en, m, j0 + jj, es, g[jj], lv[jj], rc[jj], ok);
+        };
+        if (t0 + kBM <= T) {
+#pragma unroll 1
+          for (int m = 0; m < MR; m += 2) {
+            step(m, r0, r1, true);
+            if (m + 1 < MR) step(m + 1, r1, r0, true);
+          }
+        } else {
+#pragma unroll 1
+          for (int m = 0; m < MR; m += 2) {
+            step(m, r0, r1, eok);
+            if (m + 1 < MR) step(m + 1, r1, r0, eok);
           }
         }
         fence_before();
         mbar_arrive(&tempty[buf]);
-        if (eok) {
 #pragma unroll
-          for (int jj = 0; jj < JT; ++jj) F::epi_store_l(a, en, j0 + jj, es, dl[jj]);
-        }
+        for (int jj = 0; jj < JT; ++jj) F::epi_store_l(a, en, j0 + jj, es, dl[jj], eok);
       }
     } else {
     constexpr int CPART = ((NT / (EW / 4)) + 31) / 32 * 32;

@@ -76,7 +76,8 @@ VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launche
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = os.environ.get("CANVAS_VEC_RT", "0") == "1"  # quads at a run-time 4 B offset: two 16 B loads + select (measured 1.7x slower on the layer1 GEMMs: off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
-EPI_BC = os.environ.get("CANVAS_EPI_BC", "1") == "1"  # FC dgrad epilogue applies the input broadcast's adjoint
+EPI_BC = os.environ.get("CANVAS_EPI_BC", "0") == "1"  # FC dgrad epilogue applies the input broadcast's adjoint (built + parity-tested; measured 1.10 ms vs 0.81 ms for dgrad + replica-sum on layer1: off)
+EPI_PREFETCH = os.environ.get("CANVAS_EPI_PF", "1") == "1"  # ... with the next replica's operand gathers in flight
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
 TC_WGRAD_JG_MAX = int(os.environ.get("CANVAS_WGRAD_JG", "1"))  # max row tiles per wgrad CTA (1 vs 2: +0.5% img/s on config 2 with 8192-pixel chunks)
@@ -838,7 +839,11 @@ class Fn:
         self.memo_put(key, v)
         return v
 
-    def store(self, d: TDesc, coords, val: str, beta: bool) -> None:
+    def store(self, d: TDesc, coords, val: str, beta: bool, pred: str = "") -> None:
+        if pred:  # predicated scalar store (address computed unconditionally)
+            a = self.addr(d, coords)
+            self._emit(f"if ({pred}) *({a}) = {val};")
+            return
         if self.V > 1:
             a, c = self.vec_addr(d, coords)
             if c == 0:
@@ -2259,24 +2264,30 @@ class Lowerer:
             sp = tuple(f.decompose("s", nv.sp_ext))
             return self.val(f, lhs_n, lc + sp) if need_l else "0.f"
 
+        def rhs_val(f):
+            kk = f.ivar(f"m*{L} + j")
+            rc = tuple(f.decompose(kk, at["rcore"]))
+            sp = tuple(f.decompose("s", nv.sp_ext))
+            return self.val(f, rhs_n, rc + sp) if need_r else "0.f"
+
         def term(f):
             kk = f.ivar(f"m*{L} + j")
             rc = tuple(f.decompose(kk, at["rcore"]))
             sp = tuple(f.decompose("s", nv.sp_ext))
-            r = self.val(f, rhs_n, rc + sp) if need_r else "0.f"
-            dr = f.fvar(_bc_d_rhs(op, "g", "l", r))
-            f.store(rd, rc + sp, dr, False)
-            return f.fvar(_bc_d_lhs(op, "g", "l", r))
+            dr = f.fvar(_bc_d_rhs(op, "g", "l", "r"))
+            f.store(rd, rc + sp, dr, False, pred="ok")
+            return f.fvar(_bc_d_lhs(op, "g", "l", "r"))
 
         def store_l(f):
             lc = tuple(f.decompose("j", at["lcore"]))
             sp = tuple(f.decompose("s", nv.sp_ext))
-            f.store(ld, lc + sp, "dl", False)
+            f.store(ld, lc + sp, "dl", False, pred="ok")
 
-        epi = [f"  static constexpr bool EPI_BC = true;", f"  static constexpr int EPI_M = {M}, EPI_JT = {jt};"]
+        epi = [f"  static constexpr bool EPI_BC = true, EPI_PF = {'true' if EPI_PREFETCH else 'false'};", f"  static constexpr int EPI_M = {M}, EPI_JT = {jt};"]
         epi += mk("float epi_lhs(const CanvasArgs& a, const long long n, const int j, const int s)", lhs_val, {"j"})
-        epi += mk("float epi_term(const CanvasArgs& a, const long long n, const int m, const int j, const int s, const float g, const float l)", term, {"m", "j"})
-        epi += mk("void epi_store_l(const CanvasArgs& a, const long long n, const int j, const int s, const float dl)", store_l, {"j"})
+        epi += mk("float epi_rhs(const CanvasArgs& a, const long long n, const int m, const int j, const int s)", rhs_val, {"m", "j"})
+        epi += mk("float epi_term(const CanvasArgs& a, const long long n, const int m, const int j, const int s, const float g, const float l, const float r, const bool ok)", term, {"m", "j"})
+        epi += mk("void epi_store_l(const CanvasArgs& a, const long long n, const int j, const int s, const float dl, const bool ok)", store_l, {"j"})
         self.emit_gemm_nk(name, fa, a_expr, bfn, None, M=K, K=O, S=S, phase=1, beta=BETA_NONE,
                           what=f"dgrad+bcast adjoint {K}x{O}x{S} n{u}->n{lhs_n},n{v}",
                           nbytes=4 * (nu.numel + nv.numel + self.nodes[lhs_n].numel), flops=flops, epi=(nt, epi))

@@ -219,8 +219,8 @@ void gemm_nk_epi_bc(const CanvasArgs& a) {
       const float l = F::epi_lhs(a, n, j, s);
       float dl = 0.f;
       for (int m = 0; m < F::EPI_M; ++m)
-        dl += F::epi_term(a, n, m, j, s, out[(j / F::EPI_JT) * NT + m * F::EPI_JT + j % F::EPI_JT], l);
-      F::epi_store_l(a, n, j, s, dl);
+        dl += F::epi_term(a, n, m, j, s, out[(j / F::EPI_JT) * NT + m * F::EPI_JT + j % F::EPI_JT], l, F::epi_rhs(a, n, m, j, s), true);
+      F::epi_store_l(a, n, j, s, dl, true);
     }
   }
   delete[] col;

@@ -148,3 +148,20 @@ def test_wgrad_row_groups(name, monkeypatch):
         assert_close(case, y, dx, dws, f"{name} JG=2")
     finally:
         executor._plan_cached.cache_clear()
+
+
+@pytest.mark.parametrize("cin,cout,hw,stride", [(64, 64, 16, 1), (64, 128, 16, 2), (128, 128, 8, 1)])
+def test_dgrad_bcast_epilogue(cin, cout, hw, stride, monkeypatch):
+    """The dgrad whose TMEM epilogue applies the input broadcast's adjoint
+    (CANVAS_EPI_BC=1, off by default): seed-7 #1 vs the fp64 oracle."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "EPI_BC", True)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.SEED7_K1, cin, cout, hw, hw, stride=stride, n=2)
+        assert "EPI_BC = true" in case.plan.source
+        y, dx, dws = run_gpu(case)
+        assert_close(case, y, dx, dws, f"epi-bc {cin}->{cout} {hw}^2 s{stride}")
+    finally:
+        executor._plan_cached.cache_clear()

@@ -44,14 +44,28 @@ def test_vector_producers(name, h, w):
 
 
 @pytest.mark.parametrize("cin,cout,stride", [(32, 32, 1), (32, 64, 2), (64, 32, 1)])
-def test_dgrad_bcast_epilogue(cin, cout, stride):
+def test_dgrad_bcast_epilogue(cin, cout, stride, monkeypatch):
     """seed-7 #1's K = 9C FC reads bcast(min)(n7, unfold(softmax)): its dgrad epilogue
     writes the rhs edge contribution and the replica-summed lhs gradient (no
-    materialised 9C gradient, no replica-sum launch)."""
-    case = reference(zoo.SEED7_K1, cin, cout, 6, 8, stride=stride, n=2)
-    assert "EPI_BC = true" in case.plan.source
-    assert not any(L.what == "grad n7" for L in case.plan.launches)
-    assert_close(case, *emu_run(case), f"epi-bc {cin}->{cout} s{stride}")
+    materialised dL/dv, no replica-sum launch).  Off by default (slower on the
+    B200); CANVAS_EPI_BC=1 selects it."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "EPI_BC", True)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.SEED7_K1, cin, cout, 6, 8, stride=stride, n=2)
+        assert "EPI_BC = true" in case.plan.source
+        assert not any(L.what == "grad n7" for L in case.plan.launches)
+        assert_close(case, *emu_run(case), f"epi-bc {cin}->{cout} s{stride}")
+    finally:
+        executor._plan_cached.cache_clear()
+
+
+def _epi_on():
+    from paper_2304_07741_b200 import lowering
+
+    lowering.EPI_BC = True
 
 
 def _epi_sweep(i):
@@ -72,7 +86,7 @@ def _epi_sweep(i):
 def test_dgrad_bcast_epilogue_sweep():
     """Every kernel of the first 96 of the 256-kernel sweep whose FC reads a
     broadcast (at C = 32, where its dgrad is a tensor-core GEMM)."""
-    with ProcessPoolExecutor(min(8, os.cpu_count() or 1), mp_context=multiprocessing.get_context("spawn")) as ex:
+    with ProcessPoolExecutor(min(8, os.cpu_count() or 1), mp_context=multiprocessing.get_context("spawn"), initializer=_epi_on) as ex:
         res = list(ex.map(_epi_sweep, range(96)))
     errs = [e for e, _ in res if e]
     assert not errs, errs[:5]
