@@ -1525,14 +1525,24 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
         int n, s;
         pixel(kb, okv, n, s);
 #pragma unroll
-        for (int w = 0; w < RA; ++w) F::B4ld(a, rb[w], (long long)n, s, xb[w]);
+        for (int w = 0; w < RA; ++w) {
+          // rows past J feed accumulator rows that are never stored: not gathered
+          if (j0 + warp * 4 + sub + RP * w < F::J) F::B4ld(a, rb[w], (long long)n, s, xb[w]);
+        }
 #pragma unroll
         for (int w = 0; w < RB; ++w) F::A4ld(a, ra[w], (long long)n, s, xa[w]);
       };
       auto commit_kb = [&](int kb, const float (&xb)[RA][NB], const float (&xa)[RB][NA], bool okv) {
         float va[RA][4], vb[RB][4];
 #pragma unroll
-        for (int w = 0; w < RA; ++w) F::B4cp(a, rb[w], xb[w], va[w]);
+        for (int w = 0; w < RA; ++w) {
+          if (j0 + warp * 4 + sub + RP * w < F::J) {
+            F::B4cp(a, rb[w], xb[w], va[w]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) va[w][e] = 0.f;
+          }
+        }
 #pragma unroll
         for (int w = 0; w < RB; ++w) {
           F::A4cp(a, ra[w], xa[w], vb[w]);
@@ -1558,7 +1568,14 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
         int n, s;
         pixel(kb, ok, n, s);
 #pragma unroll
-        for (int w = 0; w < RA; ++w) F::B4k(a, rb[w], (long long)n, s, va[w]);
+        for (int w = 0; w < RA; ++w) {
+          if (j0 + warp * 4 + sub + RP * w < F::J) {
+            F::B4k(a, rb[w], (long long)n, s, va[w]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) va[w][e] = 0.f;
+          }
+        }
 #pragma unroll
         for (int w = 0; w < RB; ++w) {
           F::A4k(a, ra[w], (long long)n, s, vb[w]);
@@ -1606,7 +1623,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       // columns are never stored, so only pixels past the chunk end need zeros —
       // and zeroing one operand (A, the fewer rows) zeroes their products
 #pragma unroll
-      for (int w = 0; w < RA; ++w) va[w] = F::Bk(a, rb[w], n, s);
+      for (int w = 0; w < RA; ++w) va[w] = j0 + warp + PW * w < F::J ? F::Bk(a, rb[w], n, s) : 0.f;  // rows past J: never stored
 #pragma unroll
       for (int w = 0; w < RB; ++w) {
         const float v = F::Ak(a, ra[w], n, s);

@@ -76,6 +76,10 @@ VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launche
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = os.environ.get("CANVAS_VEC_RT", "0") == "1"  # quads at a run-time 4 B offset: two 16 B loads + select (measured 1.7x slower on the layer1 GEMMs: off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
+GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
+FOLD_INLINE = int(os.environ.get("CANVAS_FOLD_INLINE", "3"))  # folds over at most this many values are evaluated inline
+PLANES_GUARDED = os.environ.get("CANVAS_PLANES_GUARDED", "0") == "1"  # plane-major launches also for guarded gathers
+VEC_SHIFTED = os.environ.get("CANVAS_VEC_SHIFTED", "0") == "1"  # quads also when most gathers sit at sub-16 B shifts
 EPI_BC = os.environ.get("CANVAS_EPI_BC", "0") == "1"  # FC dgrad epilogue applies the input broadcast's adjoint (built + parity-tested; measured 1.10 ms vs 0.81 ms for dgrad + replica-sum on layer1: off)
 EPI_PREFETCH = os.environ.get("CANVAS_EPI_PF", "1") == "1"  # ... with the next replica's operand gathers in flight
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
@@ -907,11 +911,15 @@ class Lowerer:
         self.out = g.output
         self.kernels: list[str] = []  # functor + kernel source per kernel
         # forward materialisation: reductions, contractions, input, output (module docstring)
-        self.fwd_mat = {0} | {v.id for v in self.nodes if v.op in ("fold", "softmax", "fc")} | {self.out}
+        # small folds (D <= FOLD_INLINE, e.g. a max over the K = 3 taps of an Unfold) are
+        # evaluated inline by their consumers like a pointwise node (D loads), unless
+        # replicated_pointwise finds them re-evaluated often enough to materialise
+        self.fwd_mat = {0} | {v.id for v in self.nodes if v.op in ("softmax", "fc") or (v.op == "fold" and not self.inline_fold(v))} | {self.out}
         self.fwd_mat |= self.replicated_pointwise()
         # gradients materialised in the backward: every non-view node except the
         # output (its gradient is dy) — views pull through gathers
         self.grad_mat = {0} | {v.id for v in self.nodes if v.op not in VIEW_OPS and v.id != self.out and v.op != "input"}
+        self.grad_mat -= self.inline_grads()
         self.fwd_desc: dict[int, TDesc] = {}
         self.count_desc: dict[int, TDesc] = {}
         self.grad_desc: dict[int, TDesc] = {}
@@ -941,6 +949,46 @@ class Lowerer:
         return lw
 
     # -------------------------------------------------------------- materialisation
+    def inline_grads(self) -> set:
+        """Pointwise / broadcast / small-fold nodes whose gradient is not
+        materialised: the adjoint kernels that need dL/dv evaluate it inline (a
+        pull through the consumers' adjoints), saving a launch and an HBM round
+        trip.  ge[i] = how many times one element of dL/di is evaluated per
+        element of the nearest materialised gradient below it: 1 when
+        materialised, else sum over i's input edges of (edge fan-in factor:
+        Unfold K, broadcast-LHS replicas M, fold window D) x ge[input].  A
+        gradient is inlined while ge stays below REPLICATE_MIN (same rule as the
+        forward's replicated_pointwise)."""
+        if not GRAD_INLINE:
+            return set()
+        ge = {0: 1}
+        inl = set()
+        for nd in self.nodes[1:]:
+            v = nd.id
+
+            def fac(pos):
+                if nd.op == "bcast" and pos == 0:
+                    return nd.attr["M"]
+                if nd.op == "unfold":
+                    return nd.attr["K"]
+                if nd.op == "fold":
+                    return nd.attr["D"]
+                return 1
+
+            e = sum(fac(pos) * ge.get(i, 1) for pos, i in enumerate(nd.ins)) if nd.ins else 1
+            cand = (nd.op in ("ew", "bcast") or self.inline_fold(nd)) and v != self.out and not self._grad_is_fc_alias(v)
+            if nd.op in VIEW_OPS or (cand and e < REPLICATE_MIN):
+                ge[v] = e
+                if cand:
+                    inl.add(v)
+            else:
+                ge[v] = 1
+        return inl
+
+    @staticmethod
+    def inline_fold(nd) -> bool:
+        return nd.op == "fold" and nd.attr["D"] <= FOLD_INLINE
+
     def replicated_pointwise(self) -> set:
         """Pointwise nodes worth one extra HBM round trip: those whose inline
         evaluation would be repeated >= REPLICATE_MIN times per consumer output
@@ -973,12 +1021,13 @@ class Lowerer:
             seen.add(v)
             if mat(v):
                 return 1
-            return sum(loads(i, seen) for i in self.nodes[v].ins)
+            k = self.nodes[v].attr["D"] if self.nodes[v].op == "fold" else 1
+            return k * sum(loads(i, seen) for i in self.nodes[v].ins)
 
         for v in range(len(self.nodes) - 1, 0, -1):
             nd = self.nodes[v]
             evals[v] = sum(factor(u, pos) * (1 if mat(u) else evals.get(u, 1)) for u, pos in nd.consumers) or 1
-            if nd.op in ("ew", "bcast") and v != self.out and evals[v] >= REPLICATE_MIN and loads(v) >= 2:
+            if (nd.op in ("ew", "bcast") or self.inline_fold(nd)) and v != self.out and evals[v] >= REPLICATE_MIN and loads(v) >= 2:
                 chosen.add(v)
                 evals[v] = 1
         return chosen
@@ -1087,7 +1136,22 @@ class Lowerer:
             lhs = self.val(f, nd.ins[0], self.lhs_coords(f, nd, coords))
             rhs = self.val(f, nd.ins[1], coords)
             return f.fvar(_BC_FWD[at["op"]].format(lhs, rhs))
+        if op == "fold" and self.inline_fold(nd):
+            # same order and tie rule as body_fold: acc over j = 0..D-1, first max kept
+            xs = self.fold_terms(f, v, coords)
+            if at["mode"] == "avg":
+                return f.fvar(f"({' + '.join(xs)}) / {float(at['D'])!r}f")
+            acc = f.fvar(f"({xs[0]} > -INFINITY) ? {xs[0]} : -INFINITY")
+            for x in xs[1:]:
+                acc = f.fvar(f"({x} > {acc}) ? {x} : {acc}")
+            return acc
         raise LoweringError(f"node {v} ({op}) must be materialised before it is read")
+
+    def fold_terms(self, f: Fn, v: int, coords: tuple) -> list:
+        """Input values of fold node v's window at output ``coords`` (j = 0..D-1)."""
+        nd = self.nodes[v]
+        dim, D = nd.attr["dim"], nd.attr["D"]
+        return [self.val(f, nd.ins[0], coords[:dim] + (str(j),) + coords[dim:]) for j in range(D)]
 
     def lhs_coords(self, f: Fn, nd, coords) -> tuple:
         at = nd.attr
@@ -1175,7 +1239,10 @@ class Lowerer:
             if at["mode"] == "avg":
                 return f.fvar(f"{g} / {float(D)!r}f")
             m = self.val(f, u, uc)
-            cnt = f.load(self.count_desc[u], uc)
+            if u in self.count_desc:
+                cnt = f.load(self.count_desc[u], uc)
+            else:  # inlined fold: count the ties of its window here
+                cnt = f.fvar(" + ".join(f"({x} == {m} ? 1.f : 0.f)" for x in self.fold_terms(f, u, uc)))
             x = self.val(f, v, coords)
             return f.fvar(f"{x} == {m} ? {g} / {cnt} : 0.f")
         if op == "softmax":
@@ -1305,7 +1372,7 @@ class Lowerer:
         the launch is plane-major (block-uniform channel plane, threads along pixels)."""
         planes = self.plane_split(node.ext, node.sp_ext, per_image) if node is not None else None
         functor, slots = self.functor_pointwise(name, per_image, body_fn, planes)
-        if planes is not None and "? __ldg(" in functor:
+        if planes is not None and "? __ldg(" in functor and not PLANES_GUARDED:
             # guarded (Shift / Unfold) gathers: with block-uniform channel math the
             # compiler turns the guards into branches around each load and the
             # gathers serialise (measured 0.63 -> 0.75 ms on seed-7 #1 layer1 grad n7),
@@ -1321,7 +1388,7 @@ class Lowerer:
                 # gathers mostly at sub-16 B shifts (col2im over a 9C gradient): the
                 # quad form costs occupancy without saving L1 wavefronts (measured
                 # 0.52 vs 0.57 ms on seed-7 #1 layer1 grad n1) — keep one element per thread
-                if self._fn_nld["shifted"] > self._fn_nld["aligned"]:
+                if self._fn_nld["shifted"] > self._fn_nld["aligned"] and not VEC_SHIFTED:
                     vec = None
             except VecUnsupported:
                 vec = None
