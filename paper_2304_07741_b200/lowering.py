@@ -1382,7 +1382,10 @@ class Lowerer:
         # 4 consecutive elements per thread (shared index math, one address per
         # lane-affine gather) when the elements per image / plane divide by 4
         vec = None
-        if VEC_POINTWISE and (per_image if planes is None else math.prod(planes[1])) % 4 == 0:
+        # (and enough quads to fill the GPU at the bench batch: per-pixel kernels with
+        # a long inner loop — few-output FCs, their adjoints — keep one element per
+        # thread at 14x14 and below, measured 45 vs 78 us per launch)
+        if VEC_POINTWISE and (per_image if planes is None else math.prod(planes[1])) % 4 == 0 and per_image * 256 // 4 >= SMS * 2048:
             try:
                 vec = self.functor_pointwise(name, per_image, body_fn, planes, V=4)
                 # gathers mostly at sub-16 B shifts (col2im over a 9C gradient): the

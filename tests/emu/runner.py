@@ -46,8 +46,15 @@ class EmuPlan:
         for f in self.fns:
             f.argtypes = [CanvasArgs]
 
+    PAD = 1 << 14  # NaN guard zone around every scratch tensor: a read outside a tensor poisons the result
+
     def _alloc(self, rules, n):
-        return [np.zeros(max(1, r.eval(n) // 4), np.float32) for r in rules]
+        out = []
+        for r in rules:
+            m = max(1, r.eval(n) // 4)
+            buf = np.full(m + 2 * self.PAD, np.nan, np.float32)
+            out.append(buf[self.PAD : self.PAD + m])
+        return out
 
     def run(self, phase, x, ws_list, y=None, dy=None, dx=None, dws=None, saved=None):
         """Arrays are float32 numpy, C-contiguous.  ``saved``: list per copy of per-slot arrays."""
