@@ -1058,14 +1058,18 @@ struct SmemP {
   static constexpr int B_BYTES = NT * 128;
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE;
-  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;
+  static constexpr int BYTES = BAR_OFF + (2 * STAGES + 16) * 8 + 16 + 1024;  // + up to 8 TMEM buffers' full/empty
 };
 
 template <class F, int NT, int STAGES, int PW, int EW>
 __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
   using namespace tc;
   using L = SmemP<NT, STAGES>;
-  constexpr int NCOLS = TmemCols<2 * NT>::value;
+  // TMEM accumulators: 2 (double buffer), or EPI_NBUF for the broadcast-adjoint
+  // epilogue, where EPI_WPB warpgroups share each buffer (column halves of a tile)
+  constexpr int NB = F::EPI_BC ? F::EPI_NBUF : 2;
+  static_assert(NB >= 2 && NB <= 8 && NB * NT <= 512, "TMEM buffers must fit 512 columns");
+  constexpr int NCOLS = TmemCols<NB * NT>::value;
   constexpr int KB = (F::K + kBK - 1) / kBK;
   constexpr int NCT = (F::M + NT - 1) / NT;
   constexpr int ROWS = kBK / PW;  // k-rows per producer warp per k-block
@@ -1074,9 +1078,9 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
   uint8_t* smem = align_smem(smem_raw);
   cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
   cv_u64* empty = full + STAGES;
-  cv_u64* tfull = empty + STAGES;   // [2]
-  cv_u64* tempty = tfull + 2;       // [2]
-  cv_u32* tslot = (cv_u32*)(tempty + 2);
+  cv_u64* tfull = empty + STAGES;   // [NB]
+  cv_u64* tempty = tfull + 8;       // [NB]
+  cv_u32* tslot = (cv_u32*)(tempty + 8);
   const int warp = warp_index(), lane = threadIdx.x & 31;
   const long long T = a.n * (long long)F::S;
   const long long PT = (T + kBM - 1) / kBM;
@@ -1087,9 +1091,9 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
       mbar_init(&full[i], PW * 32 + 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NB; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], (F::EPI_BC ? 4 : EW) * 32);  // EPI_BC: one warpgroup drains a tile
+      mbar_init(&tempty[i], (F::EPI_BC ? 4 * F::EPI_WPB : EW) * 32);  // EPI_BC: the buffer's warpgroups drain a tile
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1232,8 +1236,8 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
       long long g = 0;
       int it = 0;
       for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x, ++it) {
-        const int buf = it & 1;
-        if (it >= 2) mbar_wait(&tempty[buf], (cv_u32)(((it >> 1) & 1) ^ 1));
+        const int buf = it % NB;
+        if (it >= NB) mbar_wait(&tempty[buf], (cv_u32)(((it / NB) & 1) ^ 1));
         fence_after();
         const cv_u32 d = tmem + buf * NT;
         for (int kb = 0; kb < KB; ++kb, ++g) {
@@ -1283,14 +1287,19 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
       // of lhs index j0 + jj), so the thread owning a pixel row writes the rhs
       // contribution of every column and sums the lhs terms over the replicas in
       // registers.  Warpgroups take alternate tiles (= alternate TMEM buffers).
-      constexpr int JT = F::EPI_JT, MR = F::EPI_M, NWG = EW / 4;
-      static_assert(JT == 8 || JT == 16, "column group of 8 or 16");
+      // warpgroup `part` drains buffer part / WPB (tiles it = buffer mod NB) and
+      // its column share (lhs indices jj = (part % WPB) * JW .. + JW of each replica)
+      constexpr int WPB = F::EPI_WPB, JW = F::EPI_JT / WPB, MR = F::EPI_M;
+      constexpr int JT = JW;
+      static_assert(EW == 4 * NB * WPB, "EPI_BC: EW = 4 x buffers x warpgroups per buffer");
+      static_assert(JW == 8 || JW == 16, "column group of 8 or 16 per warpgroup");
+      const int mybuf = part / WPB;
       int it = 0;
       for (long long tile = blockIdx.x; tile < TILES; tile += gridDim.x, ++it) {
-        if (it % NWG != part) continue;
-        const int buf = it & 1;
+        if (it % NB != mybuf) continue;
+        const int buf = mybuf;
         const long long t0 = (tile / NCT) * kBM;
-        const int j0 = (int)(tile % NCT) * JT;
+        const int j0 = (int)(tile % NCT) * F::EPI_JT + (part % WPB) * JW;
         const long long te = t0 + q * 32 + lane;
         const bool eok = te < T;
         const long long en = eok ? te / F::S : 0;
@@ -1300,31 +1309,37 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
         // while replica m is combined (two register sets, loop unrolled by 2).
         // Rows past the batch read a clamped pixel and only their stores are
         // predicated off, so the body stays branch-free.
+        // per-pixel parts of the functors (image bases, pixel decomposition, lane
+        // pointers), once per tile; the per-column rest runs on uniform registers
+        const auto XL = F::epi_lhs_ctx(a, en, es);
+        const auto XR = F::epi_rhs_ctx(a, en, es);
+        const auto XT = F::epi_term_ctx(a, en, es);
+        const auto XS = F::epi_store_l_ctx(a, en, es);
         float lv[JT], dl[JT], r0[JT], r1[JT];
 #pragma unroll
         for (int jj = 0; jj < JT; ++jj) {
-          lv[jj] = F::epi_lhs(a, en, j0 + jj, es);
-          r0[jj] = F::epi_rhs(a, en, 0, j0 + jj, es);
+          lv[jj] = F::epi_lhs(a, XL, j0 + jj);
+          r0[jj] = F::epi_rhs(a, XR, 0, j0 + jj);
           dl[jj] = 0.f;
         }
-        mbar_wait(&tfull[buf], (cv_u32)((it >> 1) & 1));
+        mbar_wait(&tfull[buf], (cv_u32)((it / NB) & 1));
         fence_after();
         // ok: store predicate — the constant true on full tiles (no per-element branch)
         auto step = [&](int m, float (&rc)[JT], float (&rn)[JT], const bool ok) {
           if constexpr (F::EPI_PF) {
             const int mn = m + 1 < MR ? m + 1 : m;
 #pragma unroll
-            for (int jj = 0; jj < JT; ++jj) rn[jj] = F::epi_rhs(a, en, mn, j0 + jj, es);
+            for (int jj = 0; jj < JT; ++jj) rn[jj] = F::epi_rhs(a, XR, mn, j0 + jj);
           } else if (m > 0) {
 #pragma unroll
-            for (int jj = 0; jj < JT; ++jj) rc[jj] = F::epi_rhs(a, en, m, j0 + jj, es);
+            for (int jj = 0; jj < JT; ++jj) rc[jj] = F::epi_rhs(a, XR, m, j0 + jj);
           }
           float g[JT];
-          const cv_u32 ta = tmem + buf * NT + ((cv_u32)(q * 32) << 16) + m * JT;
+          const cv_u32 ta = tmem + buf * NT + ((cv_u32)(q * 32) << 16) + m * F::EPI_JT + (part % WPB) * JW;
           if constexpr (JT == 16) tmem_ld16(ta, g);
           else tmem_ld8(ta, g);
 #pragma unroll
-          for (int jj = 0; jj < JT; ++jj) dl[jj] += F::epi_term(a, en, m, j0 + jj, es, g[jj], lv[jj], rc[jj], ok);
+          for (int jj = 0; jj < JT; ++jj) dl[jj] += F::epi_term(a, XT, m, j0 + jj, g[jj], lv[jj], rc[jj], ok);
         };
         if (t0 + kBM <= T) {
 #pragma unroll 1
@@ -1342,7 +1357,7 @@ __device__ __forceinline__ void tc_gemm_pix_persistent(const CanvasArgs& a) {
         fence_before();
         mbar_arrive(&tempty[buf]);
 #pragma unroll
-        for (int jj = 0; jj < JT; ++jj) F::epi_store_l(a, en, j0 + jj, es, dl[jj], eok);
+        for (int jj = 0; jj < JT; ++jj) F::epi_store_l(a, XS, j0 + jj, dl[jj], eok);
       }
     } else {
     constexpr int CPART = ((NT / (EW / 4)) + 31) / 32 * 32;

@@ -81,6 +81,7 @@ FOLD_INLINE = int(os.environ.get("CANVAS_FOLD_INLINE", "3"))  # folds over at mo
 PLANES_GUARDED = os.environ.get("CANVAS_PLANES_GUARDED", "0") == "1"  # plane-major launches also for guarded gathers
 VEC_SHIFTED = os.environ.get("CANVAS_VEC_SHIFTED", "0") == "1"  # quads also when most gathers sit at sub-16 B shifts
 EPI_BC = os.environ.get("CANVAS_EPI_BC", "0") == "1"  # FC dgrad epilogue applies the input broadcast's adjoint (built + parity-tested; measured 1.10 ms vs 0.81 ms for dgrad + replica-sum on layer1: off)
+EPI_WPB = int(os.environ.get("CANVAS_EPI_WPB", "1"))  # epilogue warpgroups per TMEM buffer (column shares; 2 measured slower: spills at 960 threads)
 EPI_PREFETCH = os.environ.get("CANVAS_EPI_PF", "1") == "1"  # ... with the next replica's operand gathers in flight
 TC_ACC_K = int(os.environ.get("CANVAS_TC_ACC_K", "1152"))  # max reduction length per TMEM accumulator
 L2_PREFETCH = os.environ.get("CANVAS_L2_PREFETCH", "0") == "1"  # producers prefetch their source rows into L2 (measured no gain: off)
@@ -123,7 +124,7 @@ def tc_persist_cfg(nt: int) -> tuple[int, int]:
     """(stages, smem bytes) of tc_gemm_pix_persistent (must match canvas::SmemP)."""
     stage = 2 * 128 * 128 + 2 * nt * 128
     stages = max(2, min(6, (220 * 1024) // stage))
-    return stages, stages * stage + (2 * stages + 4) * 8 + 16 + 1024
+    return stages, stages * stage + (2 * stages + 16) * 8 + 16 + 1024
 
 
 def tc_smem_bytes(nt: int, stages: int) -> int:
@@ -370,6 +371,13 @@ class Fn:
         self.vec16 = False
         self.ltags: list = []
         self.cur_tag = None
+        # lane-context hoisting (the dual of ``hoist``): int / pointer values that depend
+        # only on the thread's pixel (n, s) go to ``ctx_lines`` — evaluated once per
+        # tile by the TMEM epilogue instead of once per column
+        self.ctxh = False
+        self.ctx_ok: set = set()
+        self.ctx_lines: list[str] = []
+        self.ctx_vars: list[tuple] = []  # (ctype, name)
         self.nld = {"aligned": 0, "shifted": 0, "lanes": 0}  # vector-mode load sites by kind
 
     # -- bookkeeping -----------------------------------------------------------
@@ -498,6 +506,11 @@ class Fn:
     def define(self, ctype: str, name: str, expr: str, aff=None) -> None:
         """Emit ``ctype name = expr`` — per lane when expr reads lane vars (unless
         ``aff`` = (coef, align) says it is lane-affine: then once, at lane 0)."""
+        if self.ctxh and ctype == "float* const" and all(t in self.ctx_ok for t in _IDENT.findall(expr)):
+            self.ctx_lines.append(f"{ctype} {name} = {expr};")
+            self.ctx_vars.append(("float*", name))
+            self.ctx_ok.add(name)
+            return
         if self.V > 1 and self.lane_vars(expr):
             if aff is not None:
                 self._emit(f"{ctype} {name} = {expr};")
@@ -547,7 +560,11 @@ class Fn:
             return got
         v = self.fresh("i")
         uni = bool(self.uniform) and all(t in self.uniform for t in _IDENT.findall(expr))
-        if uni and self.hoist:
+        if self.ctxh and all(t in self.ctx_ok for t in _IDENT.findall(expr)):
+            self.ctx_lines.append(f"const int {v} = {expr};")
+            self.ctx_vars.append(("int", v))
+            self.ctx_ok.add(v)
+        elif uni and self.hoist:
             self.uni_lines.append(f"const int {v} = {expr};")
             self.uni_vars.append(v)
         elif self.V > 1 and self.lane_vars(expr):
@@ -591,12 +608,20 @@ class Fn:
         b = self.fresh("b")
         # hoisted: emitted into the preamble (before any scope) by the caller
         if d.bstride * MAX_BATCH < 2**31:
-            self.pre.append(f"const int {b} = (int)n * {d.bstride};")
+            line = f"const int {b} = (int)n * {d.bstride};"
             self.al[b] = (d.bstride, 0)
             r = (self.ptr(d.slot), b)
+            ctype = "int"
         else:
-            self.pre.append(f"float* __restrict__ {b} = {self.ptr(d.slot)} + n * {d.bstride}LL;")
+            line = f"float* __restrict__ {b} = {self.ptr(d.slot)} + n * {d.bstride}LL;"
             r = (b, "")
+            ctype = "float*"
+        if self.ctxh:
+            self.ctx_lines.append(line)
+            self.ctx_vars.append((ctype, b))
+            self.ctx_ok.add(b)
+        else:
+            self.pre.append(line)
         self.bases[key] = r
         return r
 
@@ -1371,8 +1396,10 @@ class Lowerer:
         ``node``: the output node whose elements the threads map to; with H*W >= PLANES_MIN_S
         the launch is plane-major (block-uniform channel plane, threads along pixels)."""
         planes = self.plane_split(node.ext, node.sp_ext, per_image) if node is not None else None
+        planes0 = planes
         functor, slots = self.functor_pointwise(name, per_image, body_fn, planes)
-        if planes is not None and "? __ldg(" in functor and not PLANES_GUARDED:
+        guarded = planes is not None and "? __ldg(" in functor
+        if guarded and not PLANES_GUARDED:
             # guarded (Shift / Unfold) gathers: with block-uniform channel math the
             # compiler turns the guards into branches around each load and the
             # gathers serialise (measured 0.63 -> 0.75 ms on seed-7 #1 layer1 grad n7),
@@ -1399,6 +1426,12 @@ class Lowerer:
         if vec is not None:
             functor, slots = vec
             vec16 = self._fn_vec16
+        elif guarded and planes is None:
+            # one element per thread with guarded gathers: plane-major after all (the
+            # branchy guards cost less than per-thread channel math here: measured
+            # 0.49 vs 0.52 ms on seed-7 #1 layer1 grad n1; quads stay flat, above)
+            planes = planes0
+            functor, slots = self.functor_pointwise(name, per_image, body_fn, planes)
         if planes is None:
             v = POINTWISE_VEC
             block = POINTWISE_BLOCK
@@ -1916,7 +1949,7 @@ class Lowerer:
         lines += [f"  static constexpr bool SPLIT = {'true' if vec and 'B4SPLIT = true' in chr(10).join(vec) else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
-        lines += epi[1] if epi else ["  static constexpr bool EPI_BC = false;", "  static constexpr int EPI_M = 1, EPI_JT = 16;"]
+        lines += epi[1] if epi else ["  static constexpr bool EPI_BC = false;", "  static constexpr int EPI_M = 1, EPI_JT = 16, EPI_NBUF = 2, EPI_WPB = 1;"]
         tc = self.use_tc and M >= 8 and K >= 16
         if epi and not tc:
             raise LoweringError("epilogue fusion needs the tensor-core dgrad")
@@ -1964,6 +1997,9 @@ class Lowerer:
                 pstages, psmem = tc_persist_cfg(nt)
                 pw = TC_PW if K > 128 else 4  # short reductions: cheap mainloop, store-bound epilogue
                 ew = 8 if nt >= 128 else 4
+                if epi:  # one warpgroup per (TMEM buffer, column share)
+                    me = re.search(r"EPI_NBUF = (\d+), EPI_WPB = (\d+)", "\n".join(epi[1]))
+                    ew = 4 * int(me.group(1)) * int(me.group(2))
                 threads = (pw + 2 + ew) * 32
                 launcher = f'extern "C" __global__ void __launch_bounds__({threads}, 1) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_persistent<{name}_F, {nt}, {pstages}, {pw}, {ew}>(a); }}\n'
                 k = self.add_kernel(name, functor, launcher)
@@ -2317,14 +2353,25 @@ class Lowerer:
         need_l = op in ("min", "max", "mul")
         ld, rd = self.edge_desc[(v, 0)], self.edge_desc[(v, 1)]
 
-        def mk(sig, body, uni):
+        def mk(fname, rtype, params, body, uni):
+            """{fname}_ctx(a, n, s) -> {fname}X: everything of the functor that depends
+            only on the thread's pixel (image bases, pixel decomposition, lane
+            pointers), built once per tile; {fname}(a, X, params) the per-column rest."""
             f = Fn(self)
             f.pre = []
             f.computing = None
             f.local_slots = fa.local_slots
             f.uniform = set(uni)
+            f.ctxh = True
+            f.ctx_ok = {"a", "p", "n", "s"}
             ret = body(f)
-            out = [f"  static __device__ __forceinline__ {sig} {{"] + ["    " + x for x in f.pre] + f.lines
+            mem = f.ctx_vars or [("int", "unused_")]
+            out = [f"  struct {fname}X {{ " + " ".join(f"{t} {v};" for t, v in mem) + " };"]
+            out.append(f"  static __device__ __forceinline__ {fname}X {fname}_ctx(const CanvasArgs& a, const long long n, const int s) {{")
+            out += ["    " + x for x in f.ctx_lines] + [f"    {fname}X X;"] + [f"    X.{v} = {v};" if v != "unused_" else "    X.unused_ = 0;" for _, v in mem] + ["    return X;", "  }"]
+            out.append(f"  static __device__ __forceinline__ {rtype} {fname}(const CanvasArgs& a, const {fname}X& X{params}) {{")
+            out += [f"    {'float* const' if t == 'float*' else 'const int'} {v} = X.{v};" for t, v in mem if v != "unused_"]
+            out += ["    " + x for x in f.pre] + f.lines
             if ret is not None:
                 out.append(f"    return {ret};")
             return out + ["  }"]
@@ -2353,11 +2400,13 @@ class Lowerer:
             sp = tuple(f.decompose("s", nv.sp_ext))
             f.store(ld, lc + sp, "dl", False, pred="ok")
 
-        epi = [f"  static constexpr bool EPI_BC = true, EPI_PF = {'true' if EPI_PREFETCH else 'false'};", f"  static constexpr int EPI_M = {M}, EPI_JT = {jt};"]
-        epi += mk("float epi_lhs(const CanvasArgs& a, const long long n, const int j, const int s)", lhs_val, {"j"})
-        epi += mk("float epi_rhs(const CanvasArgs& a, const long long n, const int m, const int j, const int s)", rhs_val, {"m", "j"})
-        epi += mk("float epi_term(const CanvasArgs& a, const long long n, const int m, const int j, const int s, const float g, const float l, const float r, const bool ok)", term, {"m", "j"})
-        epi += mk("void epi_store_l(const CanvasArgs& a, const long long n, const int j, const int s, const float dl, const bool ok)", store_l, {"j"})
+        nbuf = max(2, min(8, 512 // nt))  # TMEM accumulators in flight (3 at N = 144)
+        epi = [f"  static constexpr bool EPI_BC = true, EPI_PF = {'true' if EPI_PREFETCH else 'false'};",
+               f"  static constexpr int EPI_M = {M}, EPI_JT = {jt}, EPI_NBUF = {nbuf}, EPI_WPB = {EPI_WPB if jt // EPI_WPB >= 8 else 1};"]
+        epi += mk("epi_lhs", "float", ", const int j", lhs_val, {"j"})
+        epi += mk("epi_rhs", "float", ", const int m, const int j", rhs_val, {"m", "j"})
+        epi += mk("epi_term", "float", ", const int m, const int j, const float g, const float l, const float r, const bool ok", term, {"m", "j"})
+        epi += mk("epi_store_l", "void", ", const int j, const float dl, const bool ok", store_l, {"j"})
         self.emit_gemm_nk(name, fa, a_expr, bfn, None, M=K, K=O, S=S, phase=1, beta=BETA_NONE,
                           what=f"dgrad+bcast adjoint {K}x{O}x{S} n{u}->n{lhs_n},n{v}",
                           nbytes=4 * (nu.numel + nv.numel + self.nodes[lhs_n].numel), flops=flops, epi=(nt, epi))

@@ -215,12 +215,16 @@ void gemm_nk_epi_bc(const CanvasArgs& a) {
       for (int k = 0; k < F::K; ++k) acc = std::fma(F::A(a, m, k), col[k], acc);
       out[m] = acc;
     }
+    const auto XL = F::epi_lhs_ctx(a, n, s);
+    const auto XR = F::epi_rhs_ctx(a, n, s);
+    const auto XT = F::epi_term_ctx(a, n, s);
+    const auto XS = F::epi_store_l_ctx(a, n, s);
     for (int j = 0; j < L; ++j) {
-      const float l = F::epi_lhs(a, n, j, s);
+      const float l = F::epi_lhs(a, XL, j);
       float dl = 0.f;
       for (int m = 0; m < F::EPI_M; ++m)
-        dl += F::epi_term(a, n, m, j, s, out[(j / F::EPI_JT) * NT + m * F::EPI_JT + j % F::EPI_JT], l, F::epi_rhs(a, n, m, j, s), true);
-      F::epi_store_l(a, n, j, s, dl, true);
+        dl += F::epi_term(a, XT, m, j, out[(j / F::EPI_JT) * NT + m * F::EPI_JT + j % F::EPI_JT], l, F::epi_rhs(a, XR, m, j), true);
+      F::epi_store_l(a, XS, j, dl, true);
     }
   }
   delete[] col;
