@@ -1676,7 +1676,9 @@ class Lowerer:
         wslot, _ = self.fc_weight_slot(u)
         io = 4 * (nu.numel + self._input_numel(nu))
         flops = 2 * O * K * S
-        if O <= SMALL_FC and nu.sp_ext and len(nu.ext) == len(nu.sp_ext) + 1 and math.prod(nu.sp_ext) >= 512:
+        if (O <= SMALL_FC or (O <= 32 and O * K <= 1024)) and nu.sp_ext and len(nu.ext) == len(nu.sp_ext) + 1 and math.prod(nu.sp_ext) >= 512:
+            # (also tiny square FCs, e.g. a MobileNetV2 1x1 target at C = 24: O*K FMAs
+            # per pixel in registers beat a 1-k-block tensor-core tile, 0.16 ms there)
             # few outputs (fc(G), fc(1), ...): one thread per pixel computes all O
             # outputs in one pass over the K inputs (the input is read once, not O
             # times); needs enough pixels to fill the GPU (H*W >= 512 per image:
@@ -2037,8 +2039,12 @@ class Lowerer:
         """dW[m][j] = sum_{t=(n,s)} A(n,m,s) * B(n,j,s): deterministic split over t + ordered reduce.
         ``trans``: the reduce writes dW transposed ([J][M]) — callers swap the operand
         roles so the costlier computed operand sits on the less padded MMA side."""
+        # tensor-core wgrad down to J = 8 rows (rows past J are never gathered) and
+        # N >= 32 columns: the SIMT fallback was 72% of a MobileNetV2 1x1 layer at
+        # C = 24 (1.56 -> 0.16 ms); wgrad_small stays for M <= 16 (faster at N = 16:
+        # 0.40 vs 0.50 ms at 16x16 over 112^2)
         small = M <= 16
-        use_tc = self.use_tc and J >= 32 and not small
+        use_tc = self.use_tc and J >= 8 and not small
         if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
             jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()), WGRAD_SMALL_JT_MAX)
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)

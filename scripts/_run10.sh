@@ -1,8 +1,7 @@
 set -x
-CANVAS_EPI_BC=1 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "epilogue or pinned" > gpurun_out/gputest.log 2>&1; echo gputest=$?
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "narrow or replication or pinned" > gpurun_out/gputest.log 2>&1; echo gputest=$?
 tail -2 gpurun_out/gputest.log
-CANVAS_EPI_BC=1 timeout 300 python scripts/kbench.py --iters 10 > gpurun_out/kbench_epi_wpb2.log 2>&1
-CANVAS_EPI_BC=1 CANVAS_EPI_WPB=1 timeout 300 python scripts/kbench.py --iters 10 > gpurun_out/kbench_epi_wpb1.log 2>&1
-CANVAS_EPI_BC=1 CANVAS_EPI_PF=0 timeout 300 python scripts/kbench.py --iters 10 > gpurun_out/kbench_epi_wpb2_nopf.log 2>&1
-timeout 300 python scripts/kbench.py --iters 10 > gpurun_out/kbench_noepi.log 2>&1
-grep -h "fwd+bwd\|dgrad9 \|grad7 \|grad1 " gpurun_out/kbench_*.log
+timeout 300 python scripts/kbench.py --cin 24 --cout 144 --hw 56 --k 1 --iters 5 > gpurun_out/kb_mb1.log 2>&1
+timeout 300 python scripts/kbench.py --cin 144 --cout 24 --hw 56 --k 1 --iters 5 > gpurun_out/kb_mb2.log 2>&1
+grep -h "fwd+bwd\|wgrad9 \|fc9 " gpurun_out/kb_mb*.log
+for m in mobilenet_v2 efficientnet_b0 resnet29; do timeout 900 python bench.py --model $m --no-cpu --steps 5 --warmup 3 2>/dev/null | tail -1 | cut -c1-200; done

@@ -32,22 +32,25 @@ def main():
     ap.add_argument("--cout", type=int, default=64)
     ap.add_argument("--hw", type=int, default=56)
     ap.add_argument("--stride", type=int, default=1)
+    ap.add_argument("--k", type=int, default=3, help="replaced conv kernel size (KH = KW)")
     ap.add_argument("--batch", type=int, default=256)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--json", default="")
     ap.add_argument("--no-tc", action="store_true")
     a = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    pk2 = os.path.join(ROOT, "profiles", "r02_peaks.json")
+    tf32_peak = json.load(open(pk2))["tf32_tcgen05_tflops_sustained"] if os.path.exists(pk2) else peaks["bf16_tflops"] / 2
     text = zoo.ALL.get(a.kernel) or open(a.kernel).read()
     if a.no_tc:
         from paper_2304_07741_b200.executor import solve_target
         from paper_2304_07741_b200.graph import build_graph
         from paper_2304_07741_b200.lowering import lower
 
-        t, asg = solve_target(text, c_in=a.cin, c_out=a.cout, h=a.hw, w=a.hw, stride=a.stride)
+        t, asg = solve_target(text, c_in=a.cin, c_out=a.cout, h=a.hw, w=a.hw, k=a.k, stride=a.stride)
         plan = lower(build_graph(t, asg), c_in=a.cin, c_out=a.cout, stride=a.stride, h_in=a.hw, w_in=a.hw, use_tc=False)
     else:
-        plan = plan_for(text, c_in=a.cin, c_out=a.cout, h=a.hw, w=a.hw, stride=a.stride)
+        plan = plan_for(text, c_in=a.cin, c_out=a.cout, h=a.hw, w=a.hw, k=a.k, stride=a.stride)
     dp = device_plan(plan, 0)
     dev = torch.device("cuda:0")
     n = a.batch
@@ -96,7 +99,7 @@ def main():
         ms = statistics.median(ts)
         gbs = L.bytes_per_image * n / (ms * 1e-3) / 1e9 if L.bytes_per_image else 0.0
         tf = L.flops_per_image * n / (ms * 1e-3) / 1e12 if L.flops_per_image else 0.0
-        rows.append({"name": L.name, "what": L.what, "ms": round(ms, 4), "GBps": round(gbs, 1), "TFLOPs": round(tf, 2), "hbm_frac": round(gbs / peaks["hbm_gbs"], 3), "tf32_frac": round(tf / (peaks["bf16_tflops"] / 2), 4)})
+        rows.append({"name": L.name, "what": L.what, "ms": round(ms, 4), "GBps": round(gbs, 1), "TFLOPs": round(tf, 2), "hbm_frac": round(gbs / peaks["hbm_gbs"], 3), "tf32_frac": round(tf / tf32_peak, 4)})
     tot = sum(r["ms"] for r in rows)
     print(f"layer {a.kernel} {a.cin}->{a.cout} {a.hw}^2 s{a.stride} batch {n}: fwd+bwd {layer_ms:.3f} ms (sum of launches {tot:.3f} ms)")
     for r in rows:

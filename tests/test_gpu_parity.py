@@ -165,3 +165,14 @@ def test_dgrad_bcast_epilogue(cin, cout, hw, stride, monkeypatch):
         assert_close(case, y, dx, dws, f"epi-bc {cin}->{cout} {hw}^2 s{stride}")
     finally:
         executor._plan_cached.cache_clear()
+
+
+@pytest.mark.parametrize("cin,cout,hw,k", [(24, 144, 14, 1), (144, 24, 14, 1), (16, 96, 16, 1), (16, 16, 12, 3), (8, 8, 12, 3)])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+def test_narrow_targets(name, cin, cout, hw, k):
+    """MobileNetV2-style narrow 1x1 targets and C = 8/16 3x3 targets: tensor-core
+    wgrad with J = 8..24 rows of the 128-row tile and N = 16 columns."""
+    case = reference(zoo.ALL[name], cin, cout, hw, hw, k=k, n=2)
+    y, dx, dws = run_gpu(case)
+    assert_close(case, y, dx, dws, f"{name} {cin}->{cout} {hw}^2 k{k}")
+

@@ -43,6 +43,14 @@ def test_vector_producers(name, h, w):
     assert_close(case, *emu_run(case), f"{name} vec {h}x{w}")
 
 
+@pytest.mark.parametrize("cin,cout,hw,k", [(24, 144, 8, 1), (144, 24, 8, 1), (16, 96, 8, 1), (8, 8, 6, 3)])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+def test_narrow_targets(name, cin, cout, hw, k):
+    """Narrow targets (MobileNetV2 1x1, C = 8): tensor-core wgrad with J < 32 rows."""
+    case = reference(zoo.ALL[name], cin, cout, hw, hw, k=k, n=2)
+    assert_close(case, *emu_run(case), f"{name} {cin}->{cout} k{k}")
+
+
 @pytest.mark.parametrize("cin,cout,stride", [(32, 32, 1), (32, 64, 2), (64, 32, 1)])
 def test_dgrad_bcast_epilogue(cin, cout, stride, monkeypatch):
     """seed-7 #1's K = 9C FC reads bcast(min)(n7, unfold(softmax)): its dgrad epilogue
