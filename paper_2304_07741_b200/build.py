@@ -99,7 +99,7 @@ def build_check(verbose: bool = False) -> Path:
     cu = BUILD / "pinned_sm100a.cu"
     cu.write_text(pinned_source())
     out = BUILD / "pinned_sm100a.cubin"
-    cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-fmad=false", "-cubin", "-I", str(CSRC / "kernels"), "-diag-suppress", "177", str(cu), "-o", str(out)]
+    cmd = [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-cubin", "-I", str(CSRC / "kernels"), "-diag-suppress", "177", str(cu), "-o", str(out)]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     log = _run(cmd)

@@ -260,15 +260,15 @@ void release_module(const std::string& key) {
 // templates, the target arch, the NVRTC version and the compile options, and
 // writes each through a per-process, per-thread temporary file renamed into
 // place, so concurrent evaluator workers never read a torn cubin.
-// --fmad=false: a node value recomputed inline in another kernel (forward values
-// inside adjoint kernels, inlined gradients) must round exactly like the copy
-// the forward stored, or max/min tie tests (x == m, App. A.6/A.8) flip; without
-// contraction every functor evaluates the same expression with the same IEEE
-// roundings in every context (explicit fmaf() calls are unaffected).
+// A node value recomputed inline in another kernel (forward values inside
+// adjoint kernels, inlined gradients) must round exactly like the copy the
+// forward stored, or max/min tie tests (x == m, App. A.6/A.8) flip: the
+// lowering emits broadcast add/sub/mul as __fadd_rn/__fsub_rn/__fmul_rn, which
+// the compiler never contracts.  CANVAS_FMAD=0 additionally compiles with
+// --fmad=false (A/B: it slows expf-heavy softmax kernels ~1.5x).
 const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--extra-device-vectorization",
                                   "-default-device", "--fmad=false"};
-// CANVAS_FMAD=1 drops the last option (measurement A/B only)
-int nvrtc_nopts() { return std::getenv("CANVAS_FMAD") && std::getenv("CANVAS_FMAD")[0] == '1' ? 5 : 6; }
+int nvrtc_nopts() { return std::getenv("CANVAS_FMAD") && std::getenv("CANVAS_FMAD")[0] == '0' ? 6 : 5; }
 #define kNvrtcNOpts nvrtc_nopts()
 
 std::string cache_name(const std::string& src) {

@@ -279,10 +279,14 @@ _EW_FWD = {
     "exp": "expf({0})",
     "neg": "(-{0})",
 }
+# forward values are recomputed inline by other kernels (adjoints, inlined
+# gradients) and compared for max/min ties (App. A.6/A.8): the round-to-nearest
+# intrinsics keep the compiler from contracting a product with a neighbouring
+# add/sub into an FMA in one context but not in another
 _BC_FWD = {
-    "add": "({0} + {1})",
-    "sub": "({0} - {1})",
-    "mul": "({0} * {1})",
+    "add": "__fadd_rn({0}, {1})",
+    "sub": "__fsub_rn({0}, {1})",
+    "mul": "__fmul_rn({0}, {1})",
     "min": "fminf({0}, {1})",
     "max": "fmaxf({0}, {1})",
 }

@@ -62,6 +62,9 @@ def main():
         "compile_ahead": pf,
         "fwd_bwd_ms_median": round(statistics.median(lat), 4) if lat else None,
         "fwd_bwd_ms_p90": round(sorted(lat)[int(0.9 * (len(lat) - 1))], 4) if lat else None,
+        "timing": "CUDA-graph replay per (plan, direction); eager launches in fwd_bwd_ms_eager_*",
+        "fwd_bwd_ms_eager_median": round(statistics.median(r.extra.get("fwd_ms_eager", 0) + r.extra.get("bwd_ms_eager", 0) for r in ok), 4) if ok else None,
+        "launches_fwd_bwd_median": statistics.median(r.extra.get("launches_fwd", 0) + r.extra.get("launches_bwd", 0) for r in ok) if ok else None,
         "plan_ms_median": round(statistics.median(r.plan_ms for r in res if r.plan_ms), 1) if ok else None,
         "errors": sorted({r.error[:120] for r in res if r.error})[:10],
     }

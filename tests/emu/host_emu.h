@@ -31,6 +31,9 @@ inline int __float_as_int(float f) {
   std::memcpy(&i, &f, 4);
   return i;
 }
+inline float __fadd_rn(float a, float b) { return a + b; }
+inline float __fsub_rn(float a, float b) { return a - b; }
+inline float __fmul_rn(float a, float b) { return a * b; }
 struct float4 {
   float x, y, z, w;
 };
