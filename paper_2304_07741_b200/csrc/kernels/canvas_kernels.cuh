@@ -47,6 +47,15 @@ __device__ __forceinline__ float* ptr_add(float* p, int off) {
   return r;
 }
 
+// the 4 consecutive words starting at word m (0..3) of the 8-word window a ++ b
+// (a quad at a run-time 4 B offset from its two aligned 16 B chunks)
+__device__ __forceinline__ float4 win4(const float4 a, const float4 b, const int m) {
+  if (m == 0) return a;
+  if (m == 1) return make_float4(a.y, a.z, a.w, b.x);
+  if (m == 2) return make_float4(a.z, a.w, b.x, b.y);
+  return make_float4(a.w, b.x, b.y, b.z);
+}
+
 // warp index of this thread, through a shuffle so the compiler can prove it
 // warp-uniform: the warp-role branches of the tcgen05 templates then stay
 // uniform and producer index math / memory descriptors live on the uniform
@@ -1449,6 +1458,31 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   cv_u32* tslot = (cv_u32*)(done + 1);
   const int warp = warp_index(), lane = threadIdx.x & 31;
 
+  // producer row grouping (F::B4CLS): the operand rows are handed to producer
+  // slots sorted by their shift class (the run-time 4 B offset of their quads),
+  // so the 4 rows a warp produces per instruction share it and the select in B4cp
+  // is warp-uniform.  Rows keep their smem position; only the producer changes.
+  constexpr bool PERM = F::VEC && F::SPLIT && F::B4CLS;
+  __shared__ int perm_s[PERM ? kBM * JG : 1];
+  __shared__ int cls_s[PERM ? kBM * JG : 1];
+  if constexpr (PERM) {
+    const int jbase = blockIdx.x * kBM * JG;
+    for (int t = threadIdx.x; t < kBM * JG; t += blockDim.x) {
+      const int jj = jbase + t;
+      cls_s[t] = jj < F::J ? F::B4cls(F::B4row(a, jj)) : (1 << 30);  // rows past J last
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kBM * JG; t += blockDim.x) {
+      const int c = cls_s[t];
+      int rank = 0;
+      for (int u = 0; u < kBM * JG; ++u) {
+        const int cu = cls_s[u];
+        rank += (cu < c) || (cu == c && u < t);
+      }
+      perm_s[rank] = t;  // published by the barrier below
+    }
+  }
+
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], PW * 32);
@@ -1478,11 +1512,18 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     static_assert((kBM * JG) % RP == 0, "row passes must tile the 128-row MMA side");
     constexpr int RA = kBM * JG / RP, RB = (NT + RP - 1) / RP;
     const int quad = lane & 7, sub = lane >> 3;
+    // operand-B row (smem row) of this thread's slot w
+    int brow[RA];
+#pragma unroll
+    for (int w = 0; w < RA; ++w) {
+      const int slot = warp * 4 + sub + RP * w;
+      brow[w] = PERM ? perm_s[slot] : slot;
+    }
     typename F::B4R rb[RA];
     typename F::A4R ra[RB];
 #pragma unroll
     for (int w = 0; w < RA; ++w) {
-      const int jj = j0 + warp * 4 + sub + RP * w;
+      const int jj = j0 + brow[w];
       rb[w] = F::B4row(a, jj < F::J ? jj : F::J - 1);
     }
 #pragma unroll
@@ -1500,7 +1541,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       uint8_t* sb_lo = sb_hi + L::B_BYTES;
 #pragma unroll
       for (int w = 0; w < RA; ++w) {
-        const int row = warp * 4 + sub + RP * w;
+        const int row = brow[w];
         const int off = row * 128 + ((quad ^ (row & 7)) << 4);
         float h[4], l[4];
 #pragma unroll
@@ -1542,7 +1583,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
 #pragma unroll
         for (int w = 0; w < RA; ++w) {
           // rows past J feed accumulator rows that are never stored: not gathered
-          if (j0 + warp * 4 + sub + RP * w < F::J) F::B4ld(a, rb[w], (long long)n, s, xb[w]);
+          if (j0 + brow[w] < F::J) F::B4ld(a, rb[w], (long long)n, s, xb[w]);
         }
 #pragma unroll
         for (int w = 0; w < RB; ++w) F::A4ld(a, ra[w], (long long)n, s, xa[w]);
@@ -1551,7 +1592,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
         float va[RA][4], vb[RB][4];
 #pragma unroll
         for (int w = 0; w < RA; ++w) {
-          if (j0 + warp * 4 + sub + RP * w < F::J) {
+          if (j0 + brow[w] < F::J) {
             F::B4cp(a, rb[w], xb[w], va[w]);
           } else {
 #pragma unroll
@@ -1584,7 +1625,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
         pixel(kb, ok, n, s);
 #pragma unroll
         for (int w = 0; w < RA; ++w) {
-          if (j0 + warp * 4 + sub + RP * w < F::J) {
+          if (j0 + brow[w] < F::J) {
             F::B4k(a, rb[w], (long long)n, s, va[w]);
           } else {
 #pragma unroll

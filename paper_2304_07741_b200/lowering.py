@@ -74,7 +74,7 @@ SMS = 148
 VEC_PRODUCERS = os.environ.get("CANVAS_VEC", "1") == "1"  # tcgen05 producers evaluate 4 consecutive pixels per thread
 VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launches: 4 consecutive elements per thread
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
-VEC_RT = os.environ.get("CANVAS_VEC_RT", "0") == "1"  # quads at a run-time 4 B offset: two 16 B loads + select (measured 1.7x slower on the layer1 GEMMs: off)
+VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
 GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
 FOLD_INLINE = int(os.environ.get("CANVAS_FOLD_INLINE", "3"))  # folds over at most this many values are evaluated inline
@@ -383,6 +383,7 @@ class Fn:
         self.ctx_lines: list[str] = []
         self.ctx_vars: list[tuple] = []  # (ctype, name)
         self.nld = {"aligned": 0, "shifted": 0, "lanes": 0}  # vector-mode load sites by kind
+        self.rt_cls: list = []  # row-context offsets of the run-time-shift quads (producer row grouping)
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -823,6 +824,10 @@ class Fn:
             else:
                 mv = self.fresh("m")
                 self._emit(f"const int {mv} = (int)((reinterpret_cast<unsigned long long>({q}) >> 2) & 3ull);")
+                # the row-context part of the offset decides m for every pixel of the
+                # row (the lane part is = 0 mod 4): a producer can group rows by it
+                _, uni_part = self.offset_parts(d, coords)
+                self.rt_cls.append(uni_part if uni_part in self.uni_vars else None)
             if static:
                 conds = []
                 for ci in ([0] if m == 0 else [0, 1]):
@@ -846,9 +851,16 @@ class Fn:
                 self._emit(f"const int {bits} = {' | '.join(parts)};")
             self.cur_tag = "s"
             w = [f"{v}q0.{x}" for x in "xyzw"] + [f"{v}q1.{x}" for x in "xyzw"]
+            if not static and VEC_RT == 2:
+                # one branch on m for the 4 lanes (warp-uniform where the producer
+                # groups rows by their shift class, tc_gemm_wgrad) instead of 12 selects
+                self._emit(f"const float4 {v}w = canvas::win4({v}q0, {v}q1, {bits} >> 4);")
+                w = [f"{v}w.{x}" for x in "xyzw"] * 2
             for e in range(4):
                 if static:
                     sel = w[m + e]
+                elif VEC_RT == 2:
+                    sel = w[e]
                 else:
                     mb = f"({bits} >> 4)"
                     sel = f"({mb} == 0 ? {w[e]} : {mb} == 1 ? {w[e + 1]} : {mb} == 2 ? {w[e + 2]} : {w[e + 3]})"
@@ -1821,6 +1833,11 @@ class Lowerer:
         out += [f"    o[{e}] = {outs[e]};" for e in range(4)]
         out.append("  }")
         out += self.split_load_compute(name, f, outs, unpack, uvar, mem)
+        # row class for producer row grouping: the run-time shifts m of the row's quads
+        cls = [c for c in dict.fromkeys(f.rt_cls) if c]
+        body = " | ".join(f"((R.{c} & 3) << {2 * i})" for i, c in enumerate(cls[:8])) if cls and None not in f.rt_cls else "0"
+        out.append(f"  static constexpr bool {name}CLS = {'true' if body != '0' else 'false'};")
+        out.append(f"  static __device__ __forceinline__ int {name}cls(const {name}R& R) {{ return {body}; }}")
         return out
 
     @staticmethod
@@ -1853,10 +1870,10 @@ class Lowerer:
         comp = [(x, t) for x, t in tagged if t in "sc"]
         used = set()
         for ln, t in comp:
-            m = re.match(r"\s*const float (\w+) = (.*);$", ln)
+            m = re.match(r"\s*const float4? (\w+) = (.*);$", ln)
             if not m:
                 return no
-            toks = set(_IDENT.findall(m.group(2)))
+            toks = set(_IDENT.findall(m.group(2))) - {"canvas", "win4"}
             bad = toks & ints - set(iw) if t == "s" else toks & ints
             if bad:
                 return no
@@ -1952,6 +1969,8 @@ class Lowerer:
         self._op_vec16 = False
         vec = self.vec_operand("B4", bfn, "k", S, fa.local_slots)
         lines += vec + [f"  static constexpr bool VEC = {'true' if vec else 'false'};"]
+        if not vec:
+            lines += ["  static constexpr bool B4CLS = false;"]
         lines += [f"  static constexpr bool SPLIT = {'true' if vec and 'B4SPLIT = true' in chr(10).join(vec) else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
@@ -2081,6 +2100,8 @@ class Lowerer:
         vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots) if va4 else []
         lines += (va4 + vb4) if vb4 else []
         lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'};"]
+        if not vb4:
+            lines += ["  static constexpr bool B4CLS = false;"]
         both = vb4 and "A4SPLIT = true" in chr(10).join(va4) and "B4SPLIT = true" in chr(10).join(vb4)
         lines += [f"  static constexpr bool SPLIT = {'true' if both else 'false'};"]
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]

@@ -38,6 +38,14 @@ struct float4 {
   float x, y, z, w;
 };
 inline float4 make_float4(float x, float y, float z, float w) { return float4{x, y, z, w}; }
+namespace canvas {
+inline float4 win4(const float4 a, const float4 b, const int m) {
+  if (m == 0) return a;
+  if (m == 1) return make_float4(a.y, a.z, a.w, b.x);
+  if (m == 2) return make_float4(a.z, a.w, b.x, b.y);
+  return make_float4(a.w, b.x, b.y, b.z);
+}
+}  // namespace canvas
 
 #define CANVAS_MAX_KSLOTS 24
 struct CanvasArgs {
