@@ -1504,7 +1504,12 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   const int j0 = blockIdx.x * kBM * JG;  // rows: input channels (JG tiles of 128)
   const int m0 = blockIdx.y * NT;        // cols: output channels
 
-  if constexpr (F::VEC) if (warp < PW) {
+  // F::NQ: the functors' quads are 4 consecutive images at one pixel (S % 4 != 0);
+  // the chunk's entries are then enumerated pixel-major (t = s * N + n) — the sum
+  // over pixels does not care about the order — which needs N % 4 == 0, else the
+  // scalar producers below run
+  const bool vec_ok = F::VEC && (!F::NQ || (a.n & 3) == 0);
+  if constexpr (F::VEC) if (warp < PW && vec_ok) {
     // 4-pixel functors: lane = (row sub-index sub = lane / 8, pixel quad = lane % 8)
     // — a warp covers 4 rows x 32 pixels per pass, each thread one 16 B swizzle
     // chunk (4 consecutive pixels) of a row.  Row contexts are fixed for the CTA.
@@ -1566,10 +1571,15 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     };
     auto pixel = [&](int kb, bool& ok, int& n, int& s) {
       const long long t = tbeg + (long long)kb * kBK + 4 * quad;
-      ok = t < tend;  // tend - tbeg is a multiple of 4 (S % 4 == 0)
+      ok = t < tend;  // tend - tbeg is a multiple of 4 (S % 4 == 0, or N % 4 == 0 under NQ)
       const int ti = (int)(ok ? t : tbeg);
-      n = ti / F::S;
-      s = ti - n * F::S;
+      if constexpr (F::NQ) {
+        s = ti / (int)a.n;
+        n = ti - s * (int)a.n;
+      } else {
+        n = ti / F::S;
+        s = ti - n * F::S;
+      }
     };
     if constexpr (F::SPLIT) {
       // software pipeline: the gathers of k-block kb+1 (raw registers, no use)
@@ -1648,7 +1658,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     }
   }
   if (warp < PW) {
-    if constexpr (!F::VEC) {
+    if (!vec_ok) {
     // lane = pixel of the 32-pixel k-block (coalesced gathers, one pixel
     // decomposition per k-block); warp w owns rows w, w+8, ... (channel index
     // math is warp-uniform); each warp writes whole 128 B swizzled rows.

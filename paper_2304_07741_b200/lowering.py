@@ -75,6 +75,7 @@ VEC_PRODUCERS = os.environ.get("CANVAS_VEC", "1") == "1"  # tcgen05 producers ev
 VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launches: 4 consecutive elements per thread
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
+VEC_NQ = os.environ.get("CANVAS_VEC_NQ", "0") == "1"  # S % 4 != 0: wgrad producers take quads of 4 images at one pixel (measured 2.7x slower at 7x7: image-strided lanes break coalescing; off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
 GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
 FOLD_INLINE = int(os.environ.get("CANVAS_FOLD_INLINE", "3"))  # folds over at most this many values are evaluated inline
@@ -378,6 +379,9 @@ class Fn:
         # lane-context hoisting (the dual of ``hoist``): int / pointer values that depend
         # only on the thread's pixel (n, s) go to ``ctx_lines`` — evaluated once per
         # tile by the TMEM epilogue instead of once per column
+        # vector mode over 4 consecutive *images* at one pixel (S % 4 != 0: pixel
+        # quads would straddle images): the image bases are the lane-affine vars
+        self.lane_n = False
         self.ctxh = False
         self.ctx_ok: set = set()
         self.ctx_lines: list[str] = []
@@ -612,6 +616,13 @@ class Fn:
             return self.bases[key]
         b = self.fresh("b")
         # hoisted: emitted into the preamble (before any scope) by the caller
+        if self.lane_n:  # lane e = image n + e: the base is lane-affine with coef = image stride
+            if d.bstride * MAX_BATCH >= 2**31:
+                raise VecUnsupported("64-bit image base")
+            self._emit(f"const int {b} = (int)n * {d.bstride};")
+            self.lanes[b] = (d.bstride, 1, 0)
+            self.bases[key] = (self.ptr(d.slot), b)
+            return self.bases[key]
         if d.bstride * MAX_BATCH < 2**31:
             line = f"const int {b} = (int)n * {d.bstride};"
             self.al[b] = (d.bstride, 0)
@@ -1798,7 +1809,7 @@ class Lowerer:
         out.append(f"  static __device__ __forceinline__ float {name}(const CanvasArgs& a, const long long n, const int {uvar}, const int s) {{ return {name}k(a, {name}row(a, {uvar}), n, s); }}")
         return out
 
-    def vec_operand(self, name: str, fn, uvar: str, S: int, local_slots: list) -> list:
+    def vec_operand(self, name: str, fn, uvar: str, S: int, local_slots: list, lane_n: bool = False) -> list:
         """4-pixel form of an operand functor (Fn vector mode): ``{name}R`` /
         ``{name}row(a, uvar)`` (its own row context) and ``{name}k(a, R, n, s, o)``
         writing pixels s .. s+3 (s a multiple of 4) to o[0..3].  The lane-invariant
@@ -1806,7 +1817,7 @@ class Lowerer:
         (h, w) split when W % 4 == 0) runs once per 4 pixels and lane-affine loads
         share one address (immediate offsets).  [] when S % 4 != 0 or the body is
         not vectorisable (the template then keeps the scalar producer)."""
-        if not VEC_PRODUCERS or S % 4:
+        if not VEC_PRODUCERS or (S % 4 and not lane_n):
             return []
         f = Fn(self)
         f.pre = []
@@ -1815,7 +1826,8 @@ class Lowerer:
         f.uniform = {uvar}
         f.hoist = True
         f.V = 4
-        f.lanes = {"s": (1, 4, 0)}
+        f.lanes = {} if lane_n else {"s": (1, 4, 0)}
+        f.lane_n = lane_n
         try:
             val = fn(f)
         except VecUnsupported:
@@ -2096,10 +2108,11 @@ class Lowerer:
         lines += self.split_operand("A", fa, aval, "m")
         lines += self.split_operand("B", fb, bval, "k")
         self._op_vec16 = False
-        va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots)
-        vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots) if va4 else []
+        nq = S % 4 != 0 and VEC_NQ  # quads over 4 images at one pixel (7x7: 49 pixels)
+        va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots, lane_n=nq)
+        vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots, lane_n=nq) if va4 else []
         lines += (va4 + vb4) if vb4 else []
-        lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'};"]
+        lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'}, NQ = {'true' if vb4 and nq else 'false'};"]
         if not vb4:
             lines += ["  static constexpr bool B4CLS = false;"]
         both = vb4 and "A4SPLIT = true" in chr(10).join(va4) and "B4SPLIT = true" in chr(10).join(vb4)

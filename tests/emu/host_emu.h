@@ -187,6 +187,11 @@ void gemm_nk_vec(const CanvasArgs& a) {
 
 template <class F>
 void gemm_wgrad_vec(const CanvasArgs& a) {
+  if constexpr (F::NQ)
+    if (a.n % 4) {  // the device template falls back to the scalar producers
+      gemm_wgrad<F>(a);
+      return;
+    }
   const long long T = a.n * (long long)F::S;
   const long long Z = (T + F::TCHUNK - 1) / F::TCHUNK;
   float* av = new float[4 * F::M];
@@ -196,8 +201,12 @@ void gemm_wgrad_vec(const CanvasArgs& a) {
     std::memset(P, 0, sizeof(float) * F::M * F::J);
     const long long te = std::min<long long>((z + 1) * F::TCHUNK, T);
     for (long long t = z * F::TCHUNK; t < te; t += 4) {
-      const long long n = t / F::S;
-      const int s = (int)(t - n * F::S);
+      long long n = t / F::S;
+      int s = (int)(t - n * F::S);
+      if constexpr (F::NQ) {  // entries pixel-major, quads of 4 images
+        s = (int)(t / a.n);
+        n = t - (long long)s * a.n;
+      }
       for (int m = 0; m < F::M; ++m) F::A4k(a, F::A4row(a, m), n, s, av + 4 * m);
       for (int j = 0; j < F::J; ++j) F::B4k(a, F::B4row(a, j), n, s, bv + 4 * j);
       for (int e = 0; e < 4; ++e)

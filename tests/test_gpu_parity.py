@@ -176,3 +176,18 @@ def test_narrow_targets(name, cin, cout, hw, k):
     y, dx, dws = run_gpu(case)
     assert_close(case, y, dx, dws, f"{name} {cin}->{cout} {hw}^2 k{k}")
 
+
+@pytest.mark.parametrize("n", [4, 2])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+def test_image_quad_wgrad(name, n, monkeypatch):
+    """ResNet stage-4 geometry (7x7, S % 4 != 0): image-quad wgrad producers (F::NQ,
+    CANVAS_VEC_NQ=1, off by default) at batch 4, the scalar fallback at batch 2."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "VEC_NQ", True)
+    executor._plan_cached.cache_clear()
+    case = reference(zoo.ALL[name], 128, 128, 7, 7, n=n)
+    executor._plan_cached.cache_clear()
+    assert "NQ = true" in case.plan.source
+    assert_close(case, *run_gpu(case), f"{name} NQ n{n}")
+

@@ -39,8 +39,24 @@ def test_vector_producers(name, h, w):
     emulated GEMMs evaluate them on pixel quads."""
     case = reference(zoo.ALL[name], 16, 16, h, w)
     if name != "seed7_k0":  # seed-7 #0 has no FC
-        assert "static constexpr bool VEC = true;" in case.plan.source
+        assert "static constexpr bool VEC = true" in case.plan.source
     assert_close(case, *emu_run(case), f"{name} vec {h}x{w}")
+
+
+@pytest.mark.parametrize("n", [4, 2])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+def test_image_quad_wgrad(name, n, monkeypatch):
+    """7x7 targets (S % 4 != 0): the wgrad producers take quads of 4 images at one
+    pixel (F::NQ, entries pixel-major; CANVAS_VEC_NQ=1, off by default); batch 2
+    exercises the scalar fallback."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "VEC_NQ", True)
+    executor._plan_cached.cache_clear()
+    case = reference(zoo.ALL[name], 32, 32, 7, 7, n=n)
+    executor._plan_cached.cache_clear()
+    assert "NQ = true" in case.plan.source
+    assert_close(case, *emu_run(case), f"{name} NQ n{n}")
 
 
 @pytest.mark.parametrize("cin,cout,hw,k", [(24, 144, 8, 1), (144, 24, 8, 1), (16, 96, 8, 1), (8, 8, 6, 3)])
