@@ -463,6 +463,12 @@ def main() -> None:
                 stage[b][1].copy_(lh, non_blocking=True)
                 ready[b].record(cs)
 
+        # the loss of every step is read back to the host too, one step behind: its
+        # D2H copy is queued after the step and the host reads step i-1's value while
+        # step i runs (a blocking .item() per step would drain the GPU queue and add
+        # the graph-launch latency to every step)
+        lhost = torch.empty(2, dtype=torch.float32).pin_memory()
+        lready = [torch.cuda.Event() for _ in range(2)]
         for b in range(2):
             free[b].record()
         prefetch(0)
@@ -475,7 +481,13 @@ def main() -> None:
             if i + 1 < e2e_steps:
                 prefetch(1 - b)
             loss = step(x, lab)
-            float(loss.item())
+            lhost[b : b + 1].copy_(loss.detach().reshape(1).float(), non_blocking=True)
+            lready[b].record()
+            if i > 0:
+                lready[1 - b].synchronize()
+                float(lhost[1 - b])
+        lready[(e2e_steps - 1) % 2].synchronize()
+        float(lhost[(e2e_steps - 1) % 2])
     else:
         for _ in range(e2e_steps):
             loss = step(xh.to(dev, non_blocking=True), lh.to(dev, non_blocking=True))
