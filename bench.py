@@ -230,7 +230,7 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def make_step(model, params, opt, world: int, bucket_mb: float = 25.0):
+def make_step(model, params, opt, world: int, bucket_mb: float = 25.0, dp: bool | None = None):
     """The training step of every arm: CE loss, backward, data-parallel gradient
     average (N > 1: bucketed all-reduce overlapped with the backward,
     paper_2304_07741_b200.dp.GradBuckets — the only collective),
@@ -239,7 +239,8 @@ def make_step(model, params, opt, world: int, bucket_mb: float = 25.0):
     bucket buffer for N > 1); ``step`` also resets the gradients."""
     from paper_2304_07741_b200.dp import GradBuckets
 
-    buckets = GradBuckets(params, world, bucket_mb) if world > 1 else None
+    dp = world > 1 if dp is None else dp
+    buckets = GradBuckets(params, world, bucket_mb, collective=dp) if dp else None
 
     def fwd_bwd_update(xb, yb):
         if buckets is not None:
@@ -304,7 +305,11 @@ def main() -> None:
         return
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # CANVAS_DP_SELFTEST=1 under torchrun with one rank: the data-parallel path
+    # (NCCL process group, bucketed all-reduce captured in the step graph, max
+    # over ranks) runs on a single GPU — its smoke test on a 1-GPU box
+    dp_on = world > 1 or ("WORLD_SIZE" in os.environ and os.environ.get("CANVAS_DP_SELFTEST") == "1")
+    if dp_on:
         dist.init_process_group("nccl", device_id=dev)
     torch.backends.cudnn.allow_tf32 = False
     torch.backends.cuda.matmul.allow_tf32 = False
@@ -320,7 +325,7 @@ def main() -> None:
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn(args.batch, *spec["input"], device=dev, generator=gen)
     lab = torch.randint(0, spec["classes"], (args.batch,), device=dev, generator=gen)
-    step, fwd_bwd_update, buckets = make_step(model, params, opt, world)
+    step, fwd_bwd_update, buckets = make_step(model, params, opt, world, dp=dp_on)
 
     t_build = time.perf_counter()
     for _ in range(args.warmup):
@@ -412,7 +417,7 @@ def main() -> None:
             torch.cuda.synchronize()
 
     clocks = Clocks(local)
-    if world > 1:
+    if dp_on:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -421,7 +426,7 @@ def main() -> None:
         step(x, lab)
     e1.record()
     torch.cuda.synchronize()
-    if world > 1:
+    if dp_on:
         dist.barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
@@ -430,7 +435,7 @@ def main() -> None:
         cnt = dp.profile_count(i)
         dp.profile(i, [])
         k_times[i] = [ea.elapsed_time(eb) for ea, eb in evs[: min(cnt, len(evs))]]
-    if world > 1:
+    if dp_on:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -439,7 +444,7 @@ def main() -> None:
     # --- e2e: batch from pinned host memory each step, loss read back each step ---
     xh = x.cpu().pin_memory()
     lh = lab.cpu().pin_memory()
-    if world > 1:
+    if dp_on:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -495,7 +500,7 @@ def main() -> None:
     e3.record()
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3) / e2e_steps
-    if world > 1:
+    if dp_on:
         t = torch.tensor([ms_e2e], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
@@ -597,7 +602,7 @@ def main() -> None:
         line["cpu_baseline"]["kind"] = "port"
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dp_on:
         dist.destroy_process_group()
 
 

@@ -27,9 +27,12 @@ import torch.distributed as dist
 
 
 class GradBuckets:
-    def __init__(self, params, world: int, bucket_mb: float = 25.0, group=None):
+    def __init__(self, params, world: int, bucket_mb: float = 25.0, group=None, collective: bool | None = None):
+        """``collective``: issue the all-reduces (default: world > 1; True at world 1
+        runs the NCCL path on one GPU — bench.py's CANVAS_DP_SELFTEST)."""
         self.params = [p for p in params if p.requires_grad]
         self.world = world
+        self.collective = world > 1 if collective is None else collective
         self.group = group
         total = sum(p.numel() for p in self.params)
         dev = self.params[0].device
@@ -78,7 +81,7 @@ class GradBuckets:
             return
         self.issued[b] = True
         s, e, _ = self.buckets[b]
-        if self.world <= 1:
+        if not self.collective:
             return
         if self.cuda:
             self.side.wait_stream(torch.cuda.current_stream(self.flat.device))
@@ -92,7 +95,7 @@ class GradBuckets:
         parameters), join the side stream, average."""
         for b in range(len(self.buckets)):
             self._issue(b)
-        if self.cuda:
+        if self.cuda and self.collective:  # join only a side stream that was forked (graph capture)
             torch.cuda.current_stream(self.flat.device).wait_stream(self.side)
         if self.world > 1:
             self.flat.div_(self.world)
