@@ -351,6 +351,12 @@ int compile_module(const std::string& src, int device, CUmodule* out) {
 }
 
 size_t align256(int64_t b) { return (size_t)((b + 255) / 256 * 256); }
+// every saved / workspace tensor sits between two guard zones, so the aligned 16 B
+// chunks around a shifted quad (vector producers) can be loaded unconditionally:
+// a chunk beyond a tensor edge by at most kGuard bytes reads the guard zone and is
+// then masked per lane (slots stay 256 B aligned)
+constexpr size_t kGuard = 16384;
+size_t slot_bytes(int64_t b) { return align256(b) + 2 * kGuard; }
 
 void* slot_ptr(const canvas_plan* p, int64_t s, int64_t copy, int64_t batch, const float* x, const float* const* w,
                float* y, const float* dy, float* dx, float* const* dw, void* saved, void* ws) {
@@ -368,14 +374,14 @@ void* slot_ptr(const canvas_plan* p, int64_t s, int64_t copy, int64_t batch, con
     size_t per_copy = 0, off = 0;
     for (size_t k = 0; k < p->saved.size(); ++k) {
       if ((int64_t)k == s) off = per_copy;
-      per_copy += align256(p->saved[k].eval(batch));
+      per_copy += slot_bytes(p->saved[k].eval(batch));
     }
-    return (char*)saved + copy * per_copy + off;
+    return (char*)saved + copy * per_copy + off + kGuard;
   }
   s -= (int64_t)p->saved.size();
   size_t off = 0;
-  for (int64_t k = 0; k < s; ++k) off += align256(p->ws[k].eval(batch));
-  return (char*)ws + off;
+  for (int64_t k = 0; k < s; ++k) off += slot_bytes(p->ws[k].eval(batch));
+  return (char*)ws + off + kGuard;
 }
 
 int run_phase(const canvas_plan* p, int phase, int64_t batch, const float* x, const float* const* w, int n_fc,
@@ -572,8 +578,8 @@ int canvas_plan_query(const canvas_plan* p, int64_t batch, size_t* fwd_workspace
                       size_t* bwd_workspace) {
   if (!p || batch < 1) return fail(CANVAS_ERR_ARGS, "bad plan/batch");
   size_t sv = 0, w = 0;
-  for (const auto& s : p->saved) sv += align256(s.eval(batch));
-  for (const auto& s : p->ws) w += align256(s.eval(batch));
+  for (const auto& s : p->saved) sv += slot_bytes(s.eval(batch));
+  for (const auto& s : p->ws) w += slot_bytes(s.eval(batch));
   if (fwd_workspace) *fwd_workspace = 0;
   if (saved_bytes) *saved_bytes = sv * (size_t)p->copies;
   if (bwd_workspace) *bwd_workspace = w;

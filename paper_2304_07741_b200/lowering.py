@@ -57,6 +57,7 @@ SAVE_OPERAND = os.environ.get("CANVAS_SAVE_OPERAND", "0") == "1"  # FC forward k
 PLANES_MIN_S = int(os.environ.get("CANVAS_PLANES_MIN_S", "128"))  # plane-major launch when H*W >= this (0 = off)
 PLANES_CTAS = int(os.environ.get("CANVAS_PLANES_CTAS", str(148 * 64)))  # CTAs of a plane-major launch (planes strided)
 GEMM_TILE = 64
+SLOT_GUARD = 16384  # bytes of guard zone on each side of every saved / workspace tensor (canvas_runtime.cpp kGuard)
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
@@ -263,7 +264,7 @@ class Plan:
     # -- helpers used by module / bench ------------------------------------------------
     def sizes(self, n: int) -> tuple[int, int, int]:
         """(saved bytes for all copies, workspace bytes, fwd workspace bytes) at batch n."""
-        al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+        al = lambda b: (b + 255) // 256 * 256 + 2 * SLOT_GUARD  # noqa: E731  (canvas_runtime.cpp slot_bytes)
         saved = sum(al(r.eval(n)) for r in self.saved) * self.copies
         ws = sum(al(r.eval(n)) for r in self.ws)
         return saved, ws, 0

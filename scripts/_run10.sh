@@ -1,8 +1,8 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "image_quad or wide or pinned" > gpurun_out/gputest.log 2>&1; echo gputest=$?
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_pinning.py -x -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; echo gputest=$?
 tail -2 gpurun_out/gputest.log
-for v in "" "CANVAS_VEC_NQ=0"; do
-echo "== $v"
-env $v timeout 300 python scripts/kbench.py --cin 512 --cout 512 --hw 7 --iters 5 2>&1 | grep -E "fwd\+bwd|wgrad9 "
-env $v timeout 300 python scripts/kbench.py --cin 256 --cout 512 --hw 14 --stride 2 --iters 5 2>&1 | grep -E "fwd\+bwd|wgrad9 "
+for i in 1 2; do
+timeout 300 python scripts/kbench.py --iters 10 > gpurun_out/kb_nbr_$i.log 2>&1
+CANVAS_VEC_NBR=0 timeout 300 python scripts/kbench.py --iters 10 > gpurun_out/kb_nonbr_$i.log 2>&1
 done
+grep -h "fwd+bwd\|fc9 \|wgrad9 \|dgrad9 " gpurun_out/kb_*.log
