@@ -65,7 +65,10 @@ void canvas_plan_destroy(canvas_plan* p);
 
 /* Buffer sizes at batch `batch`: forward scratch (always 0 in v1),
  * `saved` (forward activations kept for backward, all replicas), and
- * backward workspace. */
+ * backward workspace.  Every tensor inside `saved` / the workspace sits between
+ * two 16 KB guard zones (included in these sizes), so vectorised kernels may
+ * read whole 16-byte chunks across a tensor edge; callers just pass the start
+ * of the buffers they allocated. */
 int canvas_plan_query(const canvas_plan* p, int64_t batch, size_t* fwd_workspace, size_t* saved_bytes,
                       size_t* bwd_workspace);
 
