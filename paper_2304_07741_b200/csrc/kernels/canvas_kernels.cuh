@@ -589,6 +589,35 @@ __device__ __forceinline__ void mma_tf32(cv_u32 dtmem, cv_u64 adesc, cv_u64 bdes
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
+// A operand from tensor memory (K-major: TMEM lane = MMA row, one column per K
+// element), B from shared memory
+__device__ __forceinline__ void mma_tf32_ts(cv_u32 dtmem, cv_u32 atmem, cv_u64 bdesc, cv_u32 idesc, cv_u32 accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(dtmem),
+      "r"(atmem), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+// registers -> TMEM: 16 consecutive columns of this thread's lane (warp quadrant)
+__device__ __forceinline__ void tmem_st16(cv_u32 taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st8(cv_u32 taddr, const float* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+               "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void commit(cv_u64* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -1042,6 +1071,161 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       uint8_t* sb_hi = smem + st * L::STAGE + 2 * L::A_BYTES;
       mbar_arrive_tx(&full[st], 2 * L::B_BYTES);
       bulk_g2s(sb_hi, img + (long long)kb * 2 * L::B_BYTES, 2 * L::B_BYTES, &full[st]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == PW) {
+    fence_after();
+    tmem_free<NCOLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FC forward with the computed operand staged in TENSOR memory (tcgen05.mma with
+// A from TMEM).  The producer thread of TMEM lane r evaluates pixel t0 + r for 16
+// consecutive k of the k-block (warp w: lane quadrant w % 4, k half w / 4): every
+// gather is a 128 B coalesced warp load and the split operand goes to TMEM with
+// tcgen05.st — no shared-memory stores and no 16 B-stride lane patterns, which is
+// what bounds the shared-memory path's producers (L1/TEX).  Weights: packed
+// K-major SW128 images by bulk copy, as in tc_gemm_pix.  TMEM: NACC x NT
+// accumulator columns, then STAGES x {A_hi 32, A_lo 32} columns.
+// ---------------------------------------------------------------------------
+template <class F, int NT, int STAGES, int NACC = 1, int PW = 8>
+__device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
+  using namespace tc;
+  static_assert(PW == 4 || PW == 8 || PW == 16, "4 lane quadrants x (1, 2 or 4) k shares");
+  constexpr int KS = 32 / (PW / 4);  // k of the k-block per producer thread
+  constexpr int B_BYTES = NT * 128;
+  constexpr int ACOL = NACC * NT;  // first A column
+  constexpr int NCOLS = TmemCols<ACOL + 64 * STAGES>::value;
+  static_assert(ACOL + 64 * STAGES <= 512, "TMEM: accumulators + A stages exceed 512 columns");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem(smem_raw);
+  cv_u64* full = (cv_u64*)(smem + STAGES * 2 * B_BYTES);
+  cv_u64* empty = full + STAGES;
+  cv_u64* done = empty + STAGES;
+  cv_u32* tslot = (cv_u32*)(done + 1);
+  const int warp = warp_index(), lane = threadIdx.x & 31;
+  constexpr int KB = (F::K + kBK - 1) / kBK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], PW * 32 + 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == PW) tmem_alloc<NCOLS>(tslot);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const cv_u32 tmem = *tslot;
+
+  const long long T = a.n * (long long)F::S;
+  const long long t0 = (long long)blockIdx.x * kBM;
+  const int c0 = blockIdx.y * NT;
+  const int q = warp & 3;
+
+  if (warp < PW) {
+    const int half = warp >> 2;  // k share
+    const long long t = t0 + q * 32 + lane;  // this thread's pixel (TMEM lane q*32 + lane)
+    const bool ok = t < T;
+    const long long n = ok ? t / F::S : 0;
+    const int s = ok ? (int)(t - n * F::S) : 0;
+    const cv_u32 lane_base = tmem + ((cv_u32)(q * 32) << 16);
+    float hi[16], lo[16], v[KS];
+    auto gather = [&](int kb) {
+#pragma unroll
+      for (int i = 0; i < KS; ++i) {
+        const int k = kb * kBK + half * KS + i;
+        const int kc = k < F::K ? k : F::K - 1;
+        const float x = F::Bk(a, F::Brow(a, kc), n, s);
+        v[i] = (ok && k < F::K) ? x : 0.f;
+      }
+    };
+    gather(0);
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+#pragma unroll
+      for (int i = 0; i < KS; ++i) split_tf32(v[i], hi[i], lo[i]);
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      fence_after();
+      const cv_u32 acol = lane_base + ACOL + st * 64 + half * KS;
+      if constexpr (KS >= 16) {
+#pragma unroll
+        for (int j = 0; j < KS; j += 16) {
+          tmem_st16(acol + j, hi + j);
+          tmem_st16(acol + 32 + j, lo + j);
+        }
+      } else {
+        tmem_st8(acol, hi);
+        tmem_st8(acol + 32, lo);
+      }
+      tmem_st_wait();
+      fence_before();
+      mbar_arrive(&full[st]);
+      if (kb + 1 < KB) gather(kb + 1);
+    }
+    // epilogue: TMEM lane quadrant = q, column half = warp / 4
+    mbar_wait(done, 0);
+    fence_after();
+    const long long te = t0 + q * 32 + lane;
+    const bool eok = te < T;
+    const long long en = eok ? te / F::S : 0;
+    const int es = eok ? (int)(te - en * F::S) : 0;
+    constexpr int HALF = ((NT + 16 * (PW / 4) - 1) / (16 * (PW / 4))) * 16;
+    const int cbeg = half * HALF;
+    for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {
+      float r[16];
+      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + cc, r);
+#pragma unroll
+      for (int c2 = 1; c2 < NACC; ++c2) {
+        float u[16];
+        tmem_ld16(tmem + c2 * NT + ((cv_u32)(q * 32) << 16) + cc, u);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] += u[j];
+      }
+      if (eok) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int col = c0 + cc + j;
+          if (cc + j < NT && col < F::M) F::store(a, en, col, es, r[j]);
+        }
+      }
+    }
+  } else if (warp == PW) {
+    if (lane == 0) {
+      constexpr cv_u32 idesc = idesc_tf32(NT, false);
+      for (int kb = 0; kb < KB; ++kb) {
+        const int acc = (kb * NACC) / KB;
+        const bool fresh = kb == 0 || ((kb - 1) * NACC) / KB != acc;
+        const cv_u32 d = tmem + acc * NT;
+        const int st = kb % STAGES;
+        mbar_wait(&full[st], (kb / STAGES) & 1);
+        fence_after();
+        const cv_u32 a_hi = tmem + ACOL + st * 64;
+        const cv_u32 b_hi = smem_u32(smem + st * 2 * B_BYTES);
+        const cv_u32 b_lo = b_hi + B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 8; ++kk) {
+          mma_tf32_ts(d, a_hi + kk * 8, desc_k_sw128(b_hi + kk * 32), idesc, !(fresh && kk == 0));
+          mma_tf32_ts(d, a_hi + kk * 8, desc_k_sw128(b_lo + kk * 32), idesc, 1);
+          mma_tf32_ts(d, a_hi + 32 + kk * 8, desc_k_sw128(b_hi + kk * 32), idesc, 1);
+        }
+        commit(&empty[st]);
+      }
+      commit(done);
+    }
+  } else if (lane == 0) {
+    // packed weight tile images, one bulk copy of {hi, lo} per k-block
+    const uint8_t* img = reinterpret_cast<const uint8_t*>(F::packed(a)) + (long long)blockIdx.y * KB * 2 * B_BYTES;
+    for (int kb = 0; kb < KB; ++kb) {
+      const int st = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+      mbar_arrive_tx(&full[st], 2 * B_BYTES);
+      bulk_g2s(smem + st * 2 * B_BYTES, img + (long long)kb * 2 * B_BYTES, 2 * B_BYTES, &full[st]);
     }
   }
   fence_before();

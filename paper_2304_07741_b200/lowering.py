@@ -76,6 +76,8 @@ VEC_PRODUCERS = os.environ.get("CANVAS_VEC", "1") == "1"  # tcgen05 producers ev
 VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launches: 4 consecutive elements per thread
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
+TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares)
+TC_TMEMA = os.environ.get("CANVAS_TMEMA", "0") == "1"  # FC forward: computed operand staged in TMEM (tcgen05.mma A from TMEM; parity-green, measured 0.79 vs 0.68 ms on layer1: off)
 VEC_NQ = os.environ.get("CANVAS_VEC_NQ", "0") == "1"  # S % 4 != 0: wgrad producers take quads of 4 images at one pixel (measured 2.7x slower at 7x7: image-strided lanes break coalescing; off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
 GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
@@ -2046,6 +2048,23 @@ class Lowerer:
                 self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
                 grid = (GridRule(S * nct, 0, 128, SMS), GridRule(0, 1, 1), GridRule(0, 1, 1))
                 self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=psmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vec) and self._op_vec16))
+                return False
+            # computed operand staged in tensor memory (A from TMEM): lane = pixel, no
+            # smem stores; needs accumulators + 3 A stages (64 columns each) in TMEM
+            if TC_TMEMA and not do_save and nacc * nt + 64 * 3 <= 512:
+                tstages = 3
+                tcols = nacc * nt + 64 * tstages
+                tpair = tcols <= 256
+                tsmem = tstages * 2 * nt * 128 + (2 * tstages + 1) * 8 + 16 + 1024
+                tpw = TC_TMEMA_PW
+                tthreads = (tpw + 2) * 32
+                launcher = f'extern "C" __global__ void __launch_bounds__({tthreads}, {2 if tpair and tpw <= 8 else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_tmema<{name}_F, {nt}, {tstages}, {nacc}, {tpw}>(a); }}\n'
+                k = self.add_kernel(name, functor, launcher)
+                pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
+                total = nct * kb * nt * 32
+                self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
+                grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
+                self.p.launches.append(Launch("kernel", phase, name, k, tthreads, grid, tuple(fa.local_slots), beta, smem=tsmem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops))
                 return False
             # 2 CTAs x 8 producer warps when a 2-stage ring pairs on an SM, else 1 CTA x 16 warps
             pw = TC_PIX_PW if TC_PIX_PW else (8 if smem <= TC_SMEM_PAIR else 16)

@@ -191,3 +191,20 @@ def test_image_quad_wgrad(name, n, monkeypatch):
     assert "NQ = true" in case.plan.source
     assert_close(case, *run_gpu(case), f"{name} NQ n{n}")
 
+
+@pytest.mark.parametrize("name,cin,hw", [("seed7_k1", 64, 16), ("im2col", 128, 8), ("seed7_k1", 256, 7)])
+def test_fc_forward_tmem_a(name, cin, hw, monkeypatch):
+    """FC forward with the computed operand staged in tensor memory (tcgen05.mma
+    with A from TMEM, producers writing it with tcgen05.st; CANVAS_TMEMA=1, off by
+    default) vs the fp64 oracle."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "TC_TMEMA", True)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.ALL[name], cin, cin, hw, hw, n=2)
+        assert "tc_gemm_pix_tmema" in case.plan.source
+        assert_close(case, *run_gpu(case), f"{name} tmem-A {cin} {hw}^2")
+    finally:
+        executor._plan_cached.cache_clear()
+
