@@ -1681,10 +1681,13 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   fence_after();
   const cv_u32 tmem = *tslot;
 
-  const long long T = a.n * (long long)F::S;
+  // F::SP: the vector producers enumerate (image, pixel) over a pixel range padded
+  // to a multiple of 4 (pixels >= S are masked to zero by the functors)
+  const bool vec_ok = F::VEC && (!F::NQ || (a.n & 3) == 0);
+  const long long T = a.n * (long long)(vec_ok ? F::SP : F::S);
   const long long tbeg = (long long)blockIdx.z * F::TCHUNK;
   const long long tend = tbeg + F::TCHUNK < T ? tbeg + F::TCHUNK : T;
-  const int KB = (int)((tend - tbeg + kBK - 1) / kBK);
+  const int KB = tend > tbeg ? (int)((tend - tbeg + kBK - 1) / kBK) : 0;
   const int j0 = blockIdx.x * kBM * JG;  // rows: input channels (JG tiles of 128)
   const int m0 = blockIdx.y * NT;        // cols: output channels
 
@@ -1692,7 +1695,6 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   // the chunk's entries are then enumerated pixel-major (t = s * N + n) — the sum
   // over pixels does not care about the order — which needs N % 4 == 0, else the
   // scalar producers below run
-  const bool vec_ok = F::VEC && (!F::NQ || (a.n & 3) == 0);
   if constexpr (F::VEC) if (warp < PW && vec_ok) {
     // 4-pixel functors: lane = (row sub-index sub = lane / 8, pixel quad = lane % 8)
     // — a warp covers 4 rows x 32 pixels per pass, each thread one 16 B swizzle
@@ -1753,16 +1755,20 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       fence_async_smem();
       mbar_arrive(&full[st]);
     };
-    auto pixel = [&](int kb, bool& ok, int& n, int& s) {
+    // ok: the quad's valid lanes (bit e = pixel s + e); tend - tbeg is a multiple
+    // of 4 (S or SP % 4 == 0, or N % 4 == 0 under NQ); padded pixels s + e >= S
+    // feed zeros to the A side, so they add nothing to the sums
+    auto pixel = [&](int kb, int& ok, int& n, int& s) {
       const long long t = tbeg + (long long)kb * kBK + 4 * quad;
-      ok = t < tend;  // tend - tbeg is a multiple of 4 (S % 4 == 0, or N % 4 == 0 under NQ)
+      ok = t < tend ? 15 : 0;
       const int ti = (int)(ok ? t : tbeg);
       if constexpr (F::NQ) {
         s = ti / (int)a.n;
         n = ti - s * (int)a.n;
       } else {
-        n = ti / F::S;
-        s = ti - n * F::S;
+        n = ti / F::SP;
+        s = ti - n * F::SP;
+        if constexpr (F::SP != F::S) ok &= (1 << (F::S - s < 4 ? F::S - s : 4)) - 1;
       }
     };
     if constexpr (F::SPLIT) {
@@ -1770,8 +1776,8 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       // are issued before k-block kb is combined, split and stored
       constexpr int NB = F::B4NRAW, NA = F::A4NRAW;
       float xb0[RA][NB], xa0[RB][NA], xb1[RA][NB], xa1[RB][NA];
-      bool ok0 = false, ok1 = false;
-      auto issue = [&](int kb, float (&xb)[RA][NB], float (&xa)[RB][NA], bool& okv) {
+      int ok0 = 0, ok1 = 0;
+      auto issue = [&](int kb, float (&xb)[RA][NB], float (&xa)[RB][NA], int& okv) {
         int n, s;
         pixel(kb, okv, n, s);
 #pragma unroll
@@ -1782,7 +1788,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
 #pragma unroll
         for (int w = 0; w < RB; ++w) F::A4ld(a, ra[w], (long long)n, s, xa[w]);
       };
-      auto commit_kb = [&](int kb, const float (&xb)[RA][NB], const float (&xa)[RB][NA], bool okv) {
+      auto commit_kb = [&](int kb, const float (&xb)[RA][NB], const float (&xa)[RB][NA], int okv) {
         float va[RA][4], vb[RB][4];
 #pragma unroll
         for (int w = 0; w < RA; ++w) {
@@ -1796,9 +1802,9 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
 #pragma unroll
         for (int w = 0; w < RB; ++w) {
           F::A4cp(a, ra[w], xa[w], vb[w]);
-          const bool keep = okv && warp * 4 + sub + RP * w < NT;
+          const int keep = warp * 4 + sub + RP * w < NT ? okv : 0;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) vb[w][e] = keep ? vb[w][e] : 0.f;
+          for (int e = 0; e < 4; ++e) vb[w][e] = (keep >> e) & 1 ? vb[w][e] : 0.f;
         }
         put(kb, va, vb);
       };
@@ -1814,7 +1820,7 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
     } else {
       float va[RA][4], vb[RB][4];
       auto gather = [&](int kb) {
-        bool ok;
+        int ok;
         int n, s;
         pixel(kb, ok, n, s);
 #pragma unroll
@@ -1829,9 +1835,9 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
 #pragma unroll
         for (int w = 0; w < RB; ++w) {
           F::A4k(a, ra[w], (long long)n, s, vb[w]);
-          const bool keep = ok && warp * 4 + sub + RP * w < NT;
+          const int keep = warp * 4 + sub + RP * w < NT ? ok : 0;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) vb[w][e] = keep ? vb[w][e] : 0.f;
+          for (int e = 0; e < 4; ++e) vb[w][e] = (keep >> e) & 1 ? vb[w][e] : 0.f;
         }
       };
       if (KB > 0) gather(0);

@@ -78,6 +78,7 @@ VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B 
 VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
 TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares)
 TC_TMEMA = os.environ.get("CANVAS_TMEMA", "0") == "1"  # FC forward: computed operand staged in TMEM (tcgen05.mma A from TMEM; parity-green, measured 0.79 vs 0.68 ms on layer1: off)
+VEC_PAD = os.environ.get("CANVAS_VEC_PAD", "1") == "1"  # S % 4 != 0: wgrad producers on quads of a padded pixel range
 VEC_NQ = os.environ.get("CANVAS_VEC_NQ", "0") == "1"  # S % 4 != 0: wgrad producers take quads of 4 images at one pixel (measured 2.7x slower at 7x7: image-strided lanes break coalescing; off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
 GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
@@ -385,6 +386,9 @@ class Fn:
         # vector mode over 4 consecutive *images* at one pixel (S % 4 != 0: pixel
         # quads would straddle images): the image bases are the lane-affine vars
         self.lane_n = False
+        # vector mode over a padded pixel range (S % 4 != 0): the per-lane validity
+        # every load must also satisfy (pixels past S are padding)
+        self.lane_pred = ""
         self.ctxh = False
         self.ctx_ok: set = set()
         self.ctx_lines: list[str] = []
@@ -793,6 +797,8 @@ class Fn:
         if any(str(c) in self.raw for c in coords):
             preds = self.guard + tuple(p for p in preds if p not in self.guard)
         if self.V > 1:
+            if self.lane_pred and self.lane_pred not in preds:
+                preds = preds + (self.lane_pred,)
             return self._load_vec(d, coords, preds)
         if preds:
             return self.fvar(f"({' && '.join(preds)}) ? __ldg({self.addr(d, coords)}) : 0.f")
@@ -1812,7 +1818,7 @@ class Lowerer:
         out.append(f"  static __device__ __forceinline__ float {name}(const CanvasArgs& a, const long long n, const int {uvar}, const int s) {{ return {name}k(a, {name}row(a, {uvar}), n, s); }}")
         return out
 
-    def vec_operand(self, name: str, fn, uvar: str, S: int, local_slots: list, lane_n: bool = False) -> list:
+    def vec_operand(self, name: str, fn, uvar: str, S: int, local_slots: list, lane_n: bool = False, pad: bool = False) -> list:
         """4-pixel form of an operand functor (Fn vector mode): ``{name}R`` /
         ``{name}row(a, uvar)`` (its own row context) and ``{name}k(a, R, n, s, o)``
         writing pixels s .. s+3 (s a multiple of 4) to o[0..3].  The lane-invariant
@@ -1820,7 +1826,7 @@ class Lowerer:
         (h, w) split when W % 4 == 0) runs once per 4 pixels and lane-affine loads
         share one address (immediate offsets).  [] when S % 4 != 0 or the body is
         not vectorisable (the template then keeps the scalar producer)."""
-        if not VEC_PRODUCERS or (S % 4 and not lane_n):
+        if not VEC_PRODUCERS or (S % 4 and not lane_n and not pad):
             return []
         f = Fn(self)
         f.pre = []
@@ -1831,6 +1837,8 @@ class Lowerer:
         f.V = 4
         f.lanes = {} if lane_n else {"s": (1, 4, 0)}
         f.lane_n = lane_n
+        if pad and S % 4:
+            f.lane_pred = f"(s < {S})"
         try:
             val = fn(f)
         except VecUnsupported:
@@ -2100,6 +2108,9 @@ class Lowerer:
         # 0.40 vs 0.50 ms at 16x16 over 112^2)
         small = M <= 16
         use_tc = self.use_tc and J >= 8 and not small
+        # vector producers over a padded pixel range when S % 4 != 0 (7x7: 49 -> 52):
+        # the reduction's entries are (image, padded pixel), padding masked to zero
+        SP = -(-S // 4) * 4 if (use_tc and VEC_PAD and S % 4 and not VEC_NQ) else S
         if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
             jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()), WGRAD_SMALL_JT_MAX)
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
@@ -2107,11 +2118,11 @@ class Lowerer:
             if use_tc:  # >= ~6 CTAs per SM at batch 256 without going below 512 pixels per partial
                 tiles = -(-J // (128 * wgrad_jg(J, tc_tile(M)[0]))) * tc_tile(M)[1]
                 z = -(-(6 * SMS) // tiles)
-                tchunk = min(TC_WGRAD_TCHUNK, max(512, -(-(-(-(256 * S) // z)) // 128) * 128))
+                tchunk = min(TC_WGRAD_TCHUNK, max(512, -(-(-(-(256 * SP) // z)) // 128) * 128))
             else:
                 tchunk = max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
-        self.p.ws[k_ws] = SizeRule(4 * S * M * J, tchunk, 4 * M * J)
+        self.p.ws[k_ws] = SizeRule(4 * SP * M * J, tchunk, 4 * M * J)
         fa, fb = Fn(self), Fn(self)
         fa.pre, fb.pre = [], []
         fa.computing = fb.computing = None
@@ -2123,14 +2134,14 @@ class Lowerer:
         pslot_local = fa.ptr(-1 - k_ws)  # partials (fixed up to the real ws slot in finish())
         lines = [
             f"struct {name}_F {{",
-            f"  static constexpr int M = {M}, J = {J}, S = {S}, TCHUNK = {tchunk};",
+            f"  static constexpr int M = {M}, J = {J}, S = {S}, SP = {SP}, TCHUNK = {tchunk};",
         ]
         lines += self.split_operand("A", fa, aval, "m")
         lines += self.split_operand("B", fb, bval, "k")
         self._op_vec16 = False
         nq = S % 4 != 0 and VEC_NQ  # quads over 4 images at one pixel (7x7: 49 pixels)
-        va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots, lane_n=nq)
-        vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots, lane_n=nq) if va4 else []
+        va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots, lane_n=nq, pad=SP != S)
+        vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots, lane_n=nq, pad=SP != S) if va4 else []
         lines += (va4 + vb4) if vb4 else []
         lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'}, NQ = {'true' if vb4 and nq else 'false'};"]
         if not vb4:
@@ -2154,7 +2165,7 @@ class Lowerer:
             pair = smem <= TC_SMEM_PAIR and pw <= 8
             launcher = f'extern "C" __global__ void __launch_bounds__({threads}, {2 if pair else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_wgrad<{name}_F, {nt}, {stages}, {pw}, {jg}>(a); }}\n'
             k = self.add_kernel(name, functor, launcher)
-            grid = (GridRule(0, J, 128 * jg), GridRule(0, nct, 1), GridRule(S, 0, tchunk))
+            grid = (GridRule(0, J, 128 * jg), GridRule(0, nct, 1), GridRule(SP, 0, tchunk))
             self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vb4) and self._op_vec16))
         elif small:
             jt = min(1 << max(0, (256 // M).bit_length() - 1), WGRAD_SMALL_JT_MAX)
@@ -2172,7 +2183,7 @@ class Lowerer:
         # ordered reduction of the partials into dW
         rname = name + "_reduce"
         rsrc = (
-            f"struct {rname}_F {{ static constexpr int MJ = {M * J}, S = {S}, TCHUNK = {tchunk}, TJ = {J if trans else 0}; }};\n"
+            f"struct {rname}_F {{ static constexpr int MJ = {M * J}, S = {SP}, TCHUNK = {tchunk}, TJ = {J if trans else 0}; }};\n"
             f'extern "C" __global__ void __launch_bounds__(256) {rname}(const CanvasArgs a) {{ canvas::reduce_partials<{rname}_F>(a); }}\n'
         )
         k2 = self.add_kernel(rname, "", rsrc)

@@ -106,7 +106,7 @@ void gemm_nk(const CanvasArgs& a) {
 template <class F>
 void gemm_wgrad(const CanvasArgs& a) {
   const long long T = a.n * (long long)F::S;
-  const long long Z = (T + F::TCHUNK - 1) / F::TCHUNK;
+  const long long Z = (a.n * (long long)F::SP + F::TCHUNK - 1) / F::TCHUNK;  // reduce reads partials up to SP
   float* av = new float[F::M];
   float* bv = new float[F::J];
   for (long long z = 0; z < Z; ++z) {
@@ -192,7 +192,7 @@ void gemm_wgrad_vec(const CanvasArgs& a) {
       gemm_wgrad<F>(a);
       return;
     }
-  const long long T = a.n * (long long)F::S;
+  const long long T = a.n * (long long)F::SP;  // padded pixel range (F::SP >= S)
   const long long Z = (T + F::TCHUNK - 1) / F::TCHUNK;
   float* av = new float[4 * F::M];
   float* bv = new float[4 * F::J];
@@ -201,13 +201,17 @@ void gemm_wgrad_vec(const CanvasArgs& a) {
     std::memset(P, 0, sizeof(float) * F::M * F::J);
     const long long te = std::min<long long>((z + 1) * F::TCHUNK, T);
     for (long long t = z * F::TCHUNK; t < te; t += 4) {
-      long long n = t / F::S;
-      int s = (int)(t - n * F::S);
+      long long n = t / F::SP;
+      int s = (int)(t - n * F::SP);
       if constexpr (F::NQ) {  // entries pixel-major, quads of 4 images
         s = (int)(t / a.n);
         n = t - (long long)s * a.n;
       }
-      for (int m = 0; m < F::M; ++m) F::A4k(a, F::A4row(a, m), n, s, av + 4 * m);
+      for (int m = 0; m < F::M; ++m) {
+        F::A4k(a, F::A4row(a, m), n, s, av + 4 * m);
+        if constexpr (!F::NQ)  // padded pixels (F::SP > S) contribute zero, as on the device
+          for (int e = 0; e < 4; ++e) av[4 * m + e] = s + e < F::S ? av[4 * m + e] : 0.f;
+      }
       for (int j = 0; j < F::J; ++j) F::B4k(a, F::B4row(a, j), n, s, bv + 4 * j);
       for (int e = 0; e < 4; ++e)
         for (int m = 0; m < F::M; ++m)

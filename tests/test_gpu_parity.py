@@ -208,3 +208,13 @@ def test_fc_forward_tmem_a(name, cin, hw, monkeypatch):
     finally:
         executor._plan_cached.cache_clear()
 
+
+@pytest.mark.parametrize("cin,hw,stride,n", [(512, 7, 1, 3), (256, 14, 2, 2), (64, 5, 1, 5)])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+def test_padded_quad_wgrad(name, cin, hw, stride, n):
+    """S % 4 != 0 (ResNet stage 4, 7x7): wgrad producers on pixel quads over a
+    per-image range padded to a multiple of 4 (padding lanes masked to zero)."""
+    case = reference(zoo.ALL[name], cin, cin, hw, hw, stride=stride, n=n)
+    ho = -(-hw // stride)
+    assert f"SP = {-(-ho * ho // 4) * 4}," in case.plan.source
+    assert_close(case, *run_gpu(case), f"{name} pad {cin} {hw}^2 s{stride} n{n}")

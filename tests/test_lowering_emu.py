@@ -59,6 +59,19 @@ def test_image_quad_wgrad(name, n, monkeypatch):
     assert_close(case, *emu_run(case), f"{name} NQ n{n}")
 
 
+@pytest.mark.parametrize("hw,stride,n", [(7, 1, 2), (7, 1, 3), (14, 2, 2), (5, 1, 3)])
+@pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
+def test_padded_quad_wgrad(name, hw, stride, n):
+    """Targets with S % 4 != 0 (7x7: 49 pixels): the wgrad producers run pixel quads
+    over a range padded to SP = 52 per image (padding lanes masked, zero on the
+    output-channel side), odd batches included."""
+    case = reference(zoo.ALL[name], 32, 32, hw, hw, stride=stride, n=n)
+    ho = -(-hw // stride)
+    sp = -(-ho * ho // 4) * 4
+    assert f"SP = {sp}," in case.plan.source and "VEC = true" in case.plan.source
+    assert_close(case, *emu_run(case), f"{name} pad {hw}^2 s{stride} n{n}")
+
+
 @pytest.mark.parametrize("cin,cout,hw,k", [(24, 144, 8, 1), (144, 24, 8, 1), (16, 96, 8, 1), (8, 8, 6, 3)])
 @pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
 def test_narrow_targets(name, cin, cout, hw, k):
