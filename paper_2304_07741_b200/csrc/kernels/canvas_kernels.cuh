@@ -814,7 +814,10 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
   fence_after();
   const cv_u32 tmem = *tslot;
 
-  const long long T = a.n * (long long)F::S;
+  // SX: pixels per image of the GEMM's column space — F::SP (S rounded up to a
+  // multiple of 4) for the quad producers, whose padding columns are not stored
+  constexpr int SX = (A_MN && F::VEC) ? F::SP : F::S;
+  const long long T = a.n * (long long)SX;
   const long long t0 = (long long)blockIdx.x * kBM;
   const int c0 = blockIdx.y * NT;
 
@@ -824,12 +827,13 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
       // MN-major A, 4-pixel functor: lane owns tile pixels 4*lane .. 4*lane+3 (one
       // 16 B chunk of a swizzled row), warp w owns k-rows w*ROWS .. (warp-uniform
       // row context).  The functor shares its index math and addresses across the
-      // 4 pixels; stores are 16 B.  S % 4 == 0, so a quad never straddles images.
+      // 4 pixels; stores are 16 B.  SX % 4 == 0, so a quad never straddles images.
       constexpr int ROWS = kBK / PW;
       const long long tq = t0 + 4 * lane;
       const bool okq = tq < T;
-      const int pn = okq ? (int)(tq / F::S) : 0;
-      const int ps = okq ? (int)(tq - (long long)pn * F::S) : 0;
+      const int pn = okq ? (int)(tq / SX) : 0;
+      const int ps = okq ? (int)(tq - (long long)pn * SX) : 0;
+      const int lm = SX != F::S ? (1 << (F::S - ps < 4 ? F::S - ps : 4)) - 1 : 15;  // lanes inside the image
       auto put = [&](int kb, float (&va)[ROWS][4]) {
         const int st = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
@@ -842,10 +846,11 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
           float h[4], l[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
+            const bool oke = ok && ((lm >> e) & 1);
             if constexpr (F::SAVE_B) {
-              if (ok) F::save_b(a, (long long)pn, k, ps + e, va[q][e]);
+              if (oke) F::save_b(a, (long long)pn, k, ps + e, va[q][e]);
             }
-            split_tf32(ok ? va[q][e] : 0.f, h[e], l[e]);
+            split_tf32(oke ? va[q][e] : 0.f, h[e], l[e]);
           }
           const int off = mn_off(4 * lane, warp * ROWS + q);
           *reinterpret_cast<float4*>(sa_hi + off) = make_float4(h[0], h[1], h[2], h[3]);
@@ -1036,9 +1041,9 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
     const int q = warp & 3;
     const int tr = q * 32 + lane;  // accumulator row owned by this thread
     const long long te = t0 + tr;
-    const bool eok = te < T;
-    const long long en = eok ? te / F::S : 0;
-    const int es = eok ? (int)(te - en * F::S) : 0;
+    const long long en = te < T ? te / SX : 0;
+    const int es = te < T ? (int)(te - en * SX) : 0;
+    const bool eok = te < T && (SX == F::S || es < F::S);
     constexpr int HALF = ((NT + 16 * (PW / 4) - 1) / (16 * (PW / 4))) * 16;  // columns per warpgroup, multiple of 16
     const int cbeg = (warp >> 2) * HALF;
     for (int cc = cbeg; cc < cbeg + HALF && cc < NT; cc += 16) {

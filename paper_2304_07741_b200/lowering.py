@@ -79,6 +79,8 @@ VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B of
 TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares)
 TC_TMEMA = os.environ.get("CANVAS_TMEMA", "0") == "1"  # FC forward: computed operand staged in TMEM (tcgen05.mma A from TMEM; parity-green, measured 0.79 vs 0.68 ms on layer1: off)
 VEC_PAD = os.environ.get("CANVAS_VEC_PAD", "1") == "1"  # S % 4 != 0: wgrad producers on quads of a padded pixel range
+VEC_PAD_MIN_LOADS = int(os.environ.get("CANVAS_VEC_PAD_MIN_LOADS", "2"))
+VEC_PAD_FWD = os.environ.get("CANVAS_VEC_PAD_FWD", "0") == "1"  # same for the FC forward / dgrad quads (7x7 fwd fc: 0.524 vs 0.428 ms scalar: off)
 VEC_NQ = os.environ.get("CANVAS_VEC_NQ", "0") == "1"  # S % 4 != 0: wgrad producers take quads of 4 images at one pixel (measured 2.7x slower at 7x7: image-strided lanes break coalescing; off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
 GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
@@ -1990,15 +1992,24 @@ class Lowerer:
         ]
         lines += self.split_operand("B", fb, bval, "k")
         self._op_vec16 = False
-        vec = self.vec_operand("B4", bfn, "k", S, fa.local_slots)
-        lines += vec + [f"  static constexpr bool VEC = {'true' if vec else 'false'};"]
+        # S % 4 != 0 (7x7): the tc_gemm_pix quad producers run over a per-image pixel
+        # range padded to SP (padding columns computed from zero loads, not stored)
+        tc = self.use_tc and M >= 8 and K >= 16
+        nacc_p = 1
+        while nacc_p < 4 and K > TC_ACC_K * nacc_p:
+            nacc_p *= 2
+        pix_path = tc and not epi and not TC_TMEMA and TC_A_MN == "true" and not (TC_PERSIST and K < 4 * tc_tile(M, min(TC_NTMAX, 512 // nacc_p))[0])
+        SP = -(-S // 4) * 4 if (pix_path and VEC_PAD_FWD and S % 4) else S
+        vec = self.vec_operand("B4", bfn, "k", S, fa.local_slots, pad=SP != S)
+        if not vec:
+            SP = S
+        lines += vec + [f"  static constexpr bool VEC = {'true' if vec else 'false'};", f"  static constexpr int SP = {SP};"]
         if not vec:
             lines += ["  static constexpr bool B4CLS = false;"]
         lines += [f"  static constexpr bool SPLIT = {'true' if vec and 'B4SPLIT = true' in chr(10).join(vec) else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
         lines += epi[1] if epi else ["  static constexpr bool EPI_BC = false;", "  static constexpr int EPI_M = 1, EPI_JT = 16, EPI_NBUF = 2, EPI_WPB = 1;"]
-        tc = self.use_tc and M >= 8 and K >= 16
         if epi and not tc:
             raise LoweringError("epilogue fusion needs the tensor-core dgrad")
         nacc0 = 1
@@ -2089,7 +2100,7 @@ class Lowerer:
             pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
             total = nct * kb * nt * 32
             self.p.launches.append(Launch("kernel", phase, name + "_pack", pk, 256, (GridRule(0, total, 256, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1)), tuple(fa.local_slots), BETA_NONE, what=f"pack W tiles for {name}"))
-            grid = (GridRule(S, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
+            grid = (GridRule(SP, 0, 128), GridRule(0, nct, 1), GridRule(0, 1, 1))
             self.p.launches.append(Launch("kernel", phase, name, k, threads, grid, tuple(fa.local_slots), beta, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vec) and self._op_vec16))
             return do_save
         launcher = f'extern "C" __global__ void __launch_bounds__(256) {name}(const CanvasArgs a) {{ canvas::gemm_nk<{name}_F>(a); }}\n'
@@ -2108,9 +2119,22 @@ class Lowerer:
         # 0.40 vs 0.50 ms at 16x16 over 112^2)
         small = M <= 16
         use_tc = self.use_tc and J >= 8 and not small
+        fa, fb = Fn(self), Fn(self)
+        fa.pre, fb.pre = [], []
+        fa.computing = fb.computing = None
+        fb.local_slots = fa.local_slots
+        fa.uniform, fb.uniform = {"m"}, {"k"}  # tcgen05 wgrad producers: row per warp, lane = pixel
+        fa.hoist = fb.hoist = True
+        aval = afn(fa)
+        bval = bfn(fb)
         # vector producers over a padded pixel range when S % 4 != 0 (7x7: 49 -> 52):
-        # the reduction's entries are (image, padded pixel), padding masked to zero
-        SP = -(-S // 4) * 4 if (use_tc and VEC_PAD and S % 4 and not VEC_NQ) else S
+        # the reduction's entries are (image, padded pixel), padding masked to zero.
+        # At 7x7 the quads' loads are unaligned (4 B lane stride), so they pay off only
+        # where the scalar producers are gather-bound: >= VEC_PAD_MIN_LOADS loads per
+        # element of the (input-channel side) operand — seed-7 #1 (2 loads) 0.68 ->
+        # 0.44 ms, im2col / involution (1 load) 0.32 -> 0.39 / 0.064 -> 0.070 ms
+        nld_b = sum(ln.count("__ldg") for ln in fb.pre + fb.lines)
+        SP = -(-S // 4) * 4 if (use_tc and VEC_PAD and S % 4 and not VEC_NQ and nld_b >= VEC_PAD_MIN_LOADS) else S
         if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
             jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()), WGRAD_SMALL_JT_MAX)
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
@@ -2123,14 +2147,6 @@ class Lowerer:
                 tchunk = max(2048, -(-4096 * S // 60000) * GEMM_TILE)
         k_ws, pdesc = self._new_ws((1,))
         self.p.ws[k_ws] = SizeRule(4 * SP * M * J, tchunk, 4 * M * J)
-        fa, fb = Fn(self), Fn(self)
-        fa.pre, fb.pre = [], []
-        fa.computing = fb.computing = None
-        fb.local_slots = fa.local_slots
-        fa.uniform, fb.uniform = {"m"}, {"k"}  # tcgen05 wgrad producers: row per warp, lane = pixel
-        fa.hoist = fb.hoist = True
-        aval = afn(fa)
-        bval = bfn(fb)
         pslot_local = fa.ptr(-1 - k_ws)  # partials (fixed up to the real ws slot in finish())
         lines = [
             f"struct {name}_F {{",

@@ -164,18 +164,19 @@ void reduce_partials(const CanvasArgs& a) {
 // (A4row/A4k) on pixel quads; the emulation evaluates the operands the same way
 template <class F>
 void gemm_nk_vec(const CanvasArgs& a) {
-  const long long T = a.n * (long long)F::S;
+  const long long T = a.n * (long long)F::SP;  // padded pixel range (F::SP >= S)
   float* col = new float[4 * F::K];
   for (long long t = 0; t < T; t += 4) {
-    const long long n = t / F::S;
-    const int s = (int)(t - n * F::S);
+    const long long n = t / F::SP;
+    const int s = (int)(t - n * F::SP);
+    const int nv = std::min(4, F::S - s);  // pixels of the quad inside the image
     for (int k = 0; k < F::K; ++k) {
       const typename F::B4R R = F::B4row(a, k);
       F::B4k(a, R, n, s, col + 4 * k);
       if constexpr (F::SAVE_B)
-        for (int e = 0; e < 4; ++e) F::save_b(a, n, k, s + e, col[4 * k + e]);
+        for (int e = 0; e < nv; ++e) F::save_b(a, n, k, s + e, col[4 * k + e]);
     }
-    for (int e = 0; e < 4; ++e)
+    for (int e = 0; e < nv; ++e)
       for (int m = 0; m < F::M; ++m) {
         float acc = 0.f;
         for (int k = 0; k < F::K; ++k) acc = std::fma(F::A(a, m, k), col[4 * k + e], acc);

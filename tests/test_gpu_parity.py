@@ -192,7 +192,7 @@ def test_image_quad_wgrad(name, n, monkeypatch):
     assert_close(case, *run_gpu(case), f"{name} NQ n{n}")
 
 
-@pytest.mark.parametrize("name,cin,hw", [("seed7_k1", 64, 16), ("im2col", 128, 8), ("seed7_k1", 256, 7)])
+@pytest.mark.parametrize("name,cin,hw", [("seed7_k1", 64, 16), ("im2col", 128, 8), ("seed7_k1", 128, 7)])
 def test_fc_forward_tmem_a(name, cin, hw, monkeypatch):
     """FC forward with the computed operand staged in tensor memory (tcgen05.mma
     with A from TMEM, producers writing it with tcgen05.st; CANVAS_TMEMA=1, off by
@@ -211,10 +211,20 @@ def test_fc_forward_tmem_a(name, cin, hw, monkeypatch):
 
 @pytest.mark.parametrize("cin,hw,stride,n", [(512, 7, 1, 3), (256, 14, 2, 2), (64, 5, 1, 5)])
 @pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
-def test_padded_quad_wgrad(name, cin, hw, stride, n):
-    """S % 4 != 0 (ResNet stage 4, 7x7): wgrad producers on pixel quads over a
-    per-image range padded to a multiple of 4 (padding lanes masked to zero)."""
-    case = reference(zoo.ALL[name], cin, cin, hw, hw, stride=stride, n=n)
-    ho = -(-hw // stride)
-    assert f"SP = {-(-ho * ho // 4) * 4}," in case.plan.source
-    assert_close(case, *run_gpu(case), f"{name} pad {cin} {hw}^2 s{stride} n{n}")
+@pytest.mark.parametrize("fwd", [False, True])
+def test_padded_quad_wgrad(name, cin, hw, stride, n, fwd, monkeypatch):
+    """S % 4 != 0 (ResNet stage 4, 7x7): wgrad producers (and with CANVAS_VEC_PAD_FWD=1
+    the FC forward / dgrad producers) on pixel quads over a per-image range padded to
+    a multiple of 4 (padding lanes masked to zero / padding columns not stored)."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "VEC_PAD_MIN_LOADS", 1)
+    monkeypatch.setattr(lowering, "VEC_PAD_FWD", fwd)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.ALL[name], cin, cin, hw, hw, stride=stride, n=n)
+        ho = -(-hw // stride)
+        assert f"SP = {-(-ho * ho // 4) * 4}," in case.plan.source
+        assert_close(case, *run_gpu(case), f"{name} pad {cin} {hw}^2 s{stride} n{n} fwd={fwd}")
+    finally:
+        executor._plan_cached.cache_clear()

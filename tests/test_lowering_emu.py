@@ -61,15 +61,27 @@ def test_image_quad_wgrad(name, n, monkeypatch):
 
 @pytest.mark.parametrize("hw,stride,n", [(7, 1, 2), (7, 1, 3), (14, 2, 2), (5, 1, 3)])
 @pytest.mark.parametrize("name", ["seed7_k1", "im2col", "involution"])
-def test_padded_quad_wgrad(name, hw, stride, n):
-    """Targets with S % 4 != 0 (7x7: 49 pixels): the wgrad producers run pixel quads
-    over a range padded to SP = 52 per image (padding lanes masked, zero on the
-    output-channel side), odd batches included."""
-    case = reference(zoo.ALL[name], 32, 32, hw, hw, stride=stride, n=n)
-    ho = -(-hw // stride)
-    sp = -(-ho * ho // 4) * 4
-    assert f"SP = {sp}," in case.plan.source and "VEC = true" in case.plan.source
-    assert_close(case, *emu_run(case), f"{name} pad {hw}^2 s{stride} n{n}")
+@pytest.mark.parametrize("fwd", [False, True])
+def test_padded_quad_wgrad(name, hw, stride, n, fwd, monkeypatch):
+    """Targets with S % 4 != 0 (7x7: 49 pixels): the wgrad producers (and, with
+    CANVAS_VEC_PAD_FWD=1, off by default, the FC forward / dgrad producers) run pixel
+    quads over a range padded to SP = 52 per image (padding lanes masked, zero on the
+    output-channel side; padding columns not stored), odd batches included."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "VEC_PAD_MIN_LOADS", 1)  # every kernel, not only gather-bound ones
+    monkeypatch.setattr(lowering, "VEC_PAD_FWD", fwd)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.ALL[name], 32, 32, hw, hw, stride=stride, n=n)
+        ho = -(-hw // stride)
+        sp = -(-ho * ho // 4) * 4
+        assert f"SP = {sp}," in case.plan.source and "VEC = true" in case.plan.source
+        if fwd and name != "involution":  # involution's FCs (K = 32) take the persistent path
+            assert f"SP = {sp};" in case.plan.source
+        assert_close(case, *emu_run(case), f"{name} pad {hw}^2 s{stride} n{n} fwd={fwd}")
+    finally:
+        executor._plan_cached.cache_clear()
 
 
 @pytest.mark.parametrize("cin,cout,hw,k", [(24, 144, 8, 1), (144, 24, 8, 1), (16, 96, 8, 1), (8, 8, 6, 3)])
