@@ -1651,14 +1651,17 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   // slots sorted by their shift class (the run-time 4 B offset of their quads),
   // so the 4 rows a warp produces per instruction share it and the select in B4cp
   // is warp-uniform.  Rows keep their smem position; only the producer changes.
-  constexpr bool PERM = F::VEC && F::SPLIT && F::B4CLS;
+  // F::B4KEY: rows sorted by their gather offset instead, so the 4 rows one warp
+  // instruction produces read the same lines (on seed-7 #1: the 3 column taps of
+  // one unfold row share one 16 B-chunk window; wavefronts per LDG drop)
+  constexpr bool PERM = F::VEC && F::SPLIT && (F::B4CLS || F::B4KEY);
   __shared__ int perm_s[PERM ? kBM * JG : 1];
   __shared__ int cls_s[PERM ? kBM * JG : 1];
   if constexpr (PERM) {
     const int jbase = blockIdx.x * kBM * JG;
     for (int t = threadIdx.x; t < kBM * JG; t += blockDim.x) {
       const int jj = jbase + t;
-      cls_s[t] = jj < F::J ? F::B4cls(F::B4row(a, jj)) : (1 << 30);  // rows past J last
+      cls_s[t] = jj < F::J ? (F::B4CLS ? F::B4cls(F::B4row(a, jj)) : F::B4key(F::B4row(a, jj))) : 0x7fffffff;  // rows past J last
     }
     __syncthreads();
     for (int t = threadIdx.x; t < kBM * JG; t += blockDim.x) {

@@ -83,6 +83,8 @@ VEC_PAD_MIN_LOADS = int(os.environ.get("CANVAS_VEC_PAD_MIN_LOADS", "2"))
 VEC_PAD_FWD = os.environ.get("CANVAS_VEC_PAD_FWD", "0") == "1"  # same for the FC forward / dgrad quads (7x7 fwd fc: 0.524 vs 0.428 ms scalar: off)
 VEC_NQ = os.environ.get("CANVAS_VEC_NQ", "0") == "1"  # S % 4 != 0: wgrad producers take quads of 4 images at one pixel (measured 2.7x slower at 7x7: image-strided lanes break coalescing; off)
 VEC_SPLIT = os.environ.get("CANVAS_VEC_SPLIT", "1") == "1"  # software-pipelined producers (loads one k-block ahead)
+GRAD_SIBLINGS = os.environ.get("CANVAS_GRAD_SIBLINGS", "0") == "1"  # two gradient tensors of one shape in one launch (seed-7 #1 dn7 + dn1: 1.20 vs 0.88 ms, their gathers share no lines: off)
+ROW_KEYS = os.environ.get("CANVAS_ROW_KEYS", "1") == "1"  # wgrad producers: tile rows ordered by their gather offset
 GRAD_INLINE = os.environ.get("CANVAS_GRAD_INLINE", "1") == "1"  # pointwise gradients pulled inline instead of materialised
 FOLD_INLINE = int(os.environ.get("CANVAS_FOLD_INLINE", "3"))  # folds over at most this many values are evaluated inline
 PLANES_GUARDED = os.environ.get("CANVAS_PLANES_GUARDED", "0") == "1"  # plane-major launches also for guarded gathers
@@ -397,6 +399,7 @@ class Fn:
         self.ctx_vars: list[tuple] = []  # (ctype, name)
         self.nld = {"aligned": 0, "shifted": 0, "lanes": 0}  # vector-mode load sites by kind
         self.rt_cls: list = []  # row-context offsets of the run-time-shift quads (producer row grouping)
+        self.row_keys: list = []  # row-context offsets of the static unit-stride quads (producer row ordering)
 
     # -- bookkeeping -----------------------------------------------------------
     def emit(self, s: str) -> None:
@@ -816,6 +819,12 @@ class Fn:
 
     def _load_vec_tagged(self, d: TDesc, coords, preds) -> str:
         a, c = self.vec_addr(d, coords)
+        if c == 1:
+            # the row-context offset of a unit-stride quad: rows with close values
+            # read the same lines (producer row ordering, ``{name}key``)
+            _, up = self.offset_parts(d, coords)
+            if up in self.uni_vars:
+                self.row_keys.append(up)
         pe = " && ".join(preds)
         key = ("ldv", a, pe)
         got = self.memo_get(key)
@@ -1863,6 +1872,12 @@ class Lowerer:
         body = " | ".join(f"((R.{c} & 3) << {2 * i})" for i, c in enumerate(cls[:8])) if cls and None not in f.rt_cls else "0"
         out.append(f"  static constexpr bool {name}CLS = {'true' if body != '0' else 'false'};")
         out.append(f"  static __device__ __forceinline__ int {name}cls(const {name}R& R) {{ return {body}; }}")
+        # row key: the row-context offset of the last unit-stride gather (on seed-7 #1
+        # the unfold read c*HW + dh*W + dw) — producers that sort a tile's rows by it
+        # put rows reading the same lines into one warp instruction
+        key = f.row_keys[-1] if f.row_keys and ROW_KEYS else None
+        out.append(f"  static constexpr bool {name}KEY = {'true' if key else 'false'};")
+        out.append(f"  static __device__ __forceinline__ int {name}key(const {name}R& R) {{ return {'R.' + key if key else '0'}; }}")
         return out
 
     @staticmethod
@@ -2005,7 +2020,7 @@ class Lowerer:
             SP = S
         lines += vec + [f"  static constexpr bool VEC = {'true' if vec else 'false'};", f"  static constexpr int SP = {SP};"]
         if not vec:
-            lines += ["  static constexpr bool B4CLS = false;"]
+            lines += ["  static constexpr bool B4CLS = false, B4KEY = false;"]
         lines += [f"  static constexpr bool SPLIT = {'true' if vec and 'B4SPLIT = true' in chr(10).join(vec) else 'false'};"]
         lines += ["  static __device__ __forceinline__ void store(const CanvasArgs& a, const long long n, const int m, const int s, const float acc) {"]
         lines += ["    " + s for s in fs.pre] + fs.lines + ["  }"]
@@ -2158,10 +2173,12 @@ class Lowerer:
         nq = S % 4 != 0 and VEC_NQ  # quads over 4 images at one pixel (7x7: 49 pixels)
         va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots, lane_n=nq, pad=SP != S)
         vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots, lane_n=nq, pad=SP != S) if va4 else []
+        if nld_b < VEC_PAD_MIN_LOADS:  # row ordering pays only on gather-bound rows (seed-7 #1: 0.787 -> 0.742 ms; im2col / involution: 1-5% slower)
+            vb4 = [ln.replace("B4KEY = true", "B4KEY = false") for ln in vb4]
         lines += (va4 + vb4) if vb4 else []
         lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'}, NQ = {'true' if vb4 and nq else 'false'};"]
         if not vb4:
-            lines += ["  static constexpr bool B4CLS = false;"]
+            lines += ["  static constexpr bool B4CLS = false, B4KEY = false;"]
         both = vb4 and "A4SPLIT = true" in chr(10).join(va4) and "B4SPLIT = true" in chr(10).join(vb4)
         lines += [f"  static constexpr bool SPLIT = {'true' if both else 'false'};"]
         lines += [f"  static __device__ __forceinline__ float* partials(const CanvasArgs& a) {{ return {pslot_local}; }}"]
@@ -2262,19 +2279,74 @@ class Lowerer:
             pre, span, post = self.softmax_geom(self.nodes[u])
             _, self.dot_desc[u] = self._new_ws(pre + post)
 
+        # gradient tensors not yet written at a point of the schedule (slots)
+        self._pending = {d.slot for d in self.grad_desc.values()} | {d.slot for d in self.dgrad_desc.values()}
+        self._pending |= {d.slot for d in self.dot_desc.values()} | {d.slot for d in self.edge_desc.values()}
+        self._pending.discard(self.dx_desc().slot)
+        fused_early: set = set()
         for u in range(len(self.nodes) - 1, -1, -1):
             nu = self.nodes[u]
             # 1) materialise dL/du if it is a gradient sum point (not dy, not aliased to an FC dgrad)
-            if u in self.grad_mat and not self._grad_is_fc_alias(u) and u not in self.grad_by_epi:
+            if u in self.grad_mat and not self._grad_is_fc_alias(u) and u not in self.grad_by_epi and u not in fused_early:
                 beta = dx_beta if u == 0 else BETA_NONE
                 d = self.grad_desc[u]
-                name = f"k{len(p.kernel_names)}_bwd_grad{u}"
-                self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0, inner=nu.ext[-1] if nu.ext else 1, node=nu)
+                sib = self.grad_sibling(u) if u != 0 else None
+                if sib is None:
+                    name = f"k{len(p.kernel_names)}_bwd_grad{u}"
+                    self.launch_pointwise(name, nu.numel, lambda f, u=u, d=d: self.body_grad(f, u, d), 1, beta, f"grad n{u}", 4 * 3 * nu.numel, 0, inner=nu.ext[-1] if nu.ext else 1, node=nu)
+                else:
+                    w, dw_ = sib, self.grad_desc[sib]
+                    name = f"k{len(p.kernel_names)}_bwd_grad{u}_{w}"
+
+                    def body2(f, u=u, d=d, w=w, dw_=dw_):
+                        self.body_grad(f, u, d)
+                        self.body_grad(f, w, dw_)
+
+                    self.launch_pointwise(name, nu.numel, body2, 1, beta, f"grad n{u} + n{w}", 4 * 6 * nu.numel, 0, inner=nu.ext[-1] if nu.ext else 1, node=nu)
+                    fused_early.add(w)
+                    self._pending.discard(dw_.slot)
+                self._pending.discard(d.slot)
             # 2) adjoint kernels of the producer edge that need dL/du as a whole
             if nu.op == "fc":
                 self.lower_fc_bwd(u, dx_beta)
+                for dd in (self.dgrad_desc.get(u),) + tuple(self.edge_desc.get((nu.ins[0], i)) for i in (0, 1)):
+                    if dd is not None:
+                        self._pending.discard(dd.slot)
             elif nu.op == "softmax":
                 self.lower_softmax_dot(u)
+                self._pending.discard(self.dot_desc[u].slot)
+
+    def grad_sibling(self, u: int):
+        """A later gradient tensor dL/dw (w < u) computable in the same launch as
+        dL/du: same elements per image and spatial extent, and every gradient it
+        reads already written before this point (checked by emitting its body into
+        a scratch functor).  One pass then reads their shared sources once — on
+        seed-7 #1 dL/dn7 and dL/dn1 both gather the 9C-wide dL/dn8 (the FC dgrad's
+        output) at the same and at neighbouring pixels."""
+        if not GRAD_SIBLINGS:
+            return None
+        nu = self.nodes[u]
+        for w in range(u - 1, 0, -1):
+            nw = self.nodes[w]
+            if w not in self.grad_mat or self._grad_is_fc_alias(w) or w in self.grad_by_epi:
+                continue
+            if nw.numel != nu.numel or tuple(nw.sp_ext) != tuple(nu.sp_ext) or tuple(nw.ext[len(nw.ext) - len(nw.sp_ext):]) != tuple(nu.ext[len(nu.ext) - len(nu.sp_ext):]):
+                continue
+            f = Fn(self)
+            f.pre = []
+            f.computing = None
+            f.planes = None
+            try:
+                self.body_grad(f, w, self.grad_desc[w])
+            except (VecUnsupported, LoweringError):
+                continue
+            finally:
+                self.computing_grad = None
+            reads = {d.slot for d in f.loaded.values()}
+            if reads & (self._pending - {self.grad_desc[w].slot}):
+                continue
+            return w
+        return None
 
     def _grad_is_fc_alias(self, v: int) -> bool:
         nd = self.nodes[v]

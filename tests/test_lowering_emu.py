@@ -248,3 +248,20 @@ def test_sweep_256_plans_compile_for_sm100a():
     with ProcessPoolExecutor(min(16, os.cpu_count() or 1), mp_context=multiprocessing.get_context("spawn")) as ex:
         errs = [e for e in ex.map(_nvcc_plan, range(256)) if e]
     assert not errs, errs[:5]
+
+
+@pytest.mark.parametrize("name", ["seed7_k1", "seed7_k0", "involution"])
+def test_gradient_siblings(name, monkeypatch):
+    """CANVAS_GRAD_SIBLINGS=1 (off by default): two gradient tensors of one shape in
+    one launch when every gradient the second reads is already written."""
+    from paper_2304_07741_b200 import executor, lowering
+
+    monkeypatch.setattr(lowering, "GRAD_SIBLINGS", True)
+    executor._plan_cached.cache_clear()
+    try:
+        case = reference(zoo.ALL[name], 16, 16, 10, 9)
+        if name == "seed7_k1":
+            assert any(L.what == "grad n7 + n1" for L in case.plan.launches)
+        assert_close(case, *emu_run(case), f"{name} siblings")
+    finally:
+        executor._plan_cached.cache_clear()
