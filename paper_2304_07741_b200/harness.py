@@ -167,7 +167,17 @@ class Dispatcher:
 
     def run(self, tasks: list[HarnessTask], timeout_s: float = 3600.0) -> Leaderboard:
         ctx = mp.get_context("spawn")
-        rq = ctx.Queue()
+        # results: a SimpleQueue, whose put writes the pipe synchronously in the
+        # worker's own thread — a worker that dies (os._exit, a fault) after a put
+        # cannot leave a half-flushed message or a held feeder-thread write lock
+        # behind, which with mp.Queue can stall every other worker's reports
+        rq = ctx.SimpleQueue()
+
+        def rq_get(timeout: float):
+            if not rq._reader.poll(timeout):
+                raise queue.Empty
+            return rq.get()
+
         pending = {t.task_id: t for t in tasks}
         todo = collections.deque(tasks)
         procs: dict[int, tuple] = {}  # worker id -> (process, inbox)
@@ -202,7 +212,7 @@ class Dispatcher:
             ready: set = set()
             while len(ready) < len(first) and time.monotonic() < deadline:
                 try:
-                    m = rq.get(timeout=0.2)
+                    m = rq_get(0.2)
                 except queue.Empty:
                     if any(not procs[w][0].is_alive() for w in first):
                         break
@@ -224,7 +234,7 @@ class Dispatcher:
                 if not inflight and not todo:
                     break
                 try:
-                    m = early.pop() if early else rq.get(timeout=0.2)
+                    m = early.pop() if early else rq_get(0.2)
                 except queue.Empty:
                     continue
                 if m["type"] == "ready":
