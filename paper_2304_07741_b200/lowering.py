@@ -2173,7 +2173,7 @@ class Lowerer:
         nq = S % 4 != 0 and VEC_NQ  # quads over 4 images at one pixel (7x7: 49 pixels)
         va4 = self.vec_operand("A4", afn, "m", S, fa.local_slots, lane_n=nq, pad=SP != S)
         vb4 = self.vec_operand("B4", bfn, "k", S, fa.local_slots, lane_n=nq, pad=SP != S) if va4 else []
-        if nld_b < VEC_PAD_MIN_LOADS:  # row ordering pays only on gather-bound rows (seed-7 #1: 0.787 -> 0.742 ms; im2col / involution: 1-5% slower)
+        if nld_b < VEC_PAD_MIN_LOADS or SP != S:  # row ordering pays only on gather-bound rows (seed-7 #1: 0.787 -> 0.742 ms; im2col / involution: 1-5% slower; 7x7 padded quads: 0.44 -> 0.48 ms)
             vb4 = [ln.replace("B4KEY = true", "B4KEY = false") for ln in vb4]
         lines += (va4 + vb4) if vb4 else []
         lines += [f"  static constexpr bool VEC = {'true' if vb4 else 'false'}, NQ = {'true' if vb4 and nq else 'false'};"]
