@@ -468,12 +468,14 @@ def main() -> None:
                 stage[b][1].copy_(lh, non_blocking=True)
                 ready[b].record(cs)
 
-        # the loss of every step is read back to the host too, one step behind: its
-        # D2H copy is queued after the step and the host reads step i-1's value while
-        # step i runs (a blocking .item() per step would drain the GPU queue and add
-        # the graph-launch latency to every step)
-        lhost = torch.empty(2, dtype=torch.float32).pin_memory()
-        lready = [torch.cuda.Event() for _ in range(2)]
+        # the loss of every step is read back to the host too, two steps behind: its
+        # D2H copy is queued after the step and the host reads step i-2's value while
+        # steps i-1 and i are queued (a blocking .item() per step would drain the GPU
+        # queue and add the graph-launch latency to every step; one step of slack
+        # left the GPU idle whenever the host thread was descheduled)
+        LAG = 2
+        lhost = torch.empty(LAG + 1, dtype=torch.float32).pin_memory()
+        lready = [torch.cuda.Event() for _ in range(LAG + 1)]
         for b in range(2):
             free[b].record()
         prefetch(0)
@@ -486,13 +488,16 @@ def main() -> None:
             if i + 1 < e2e_steps:
                 prefetch(1 - b)
             loss = step(x, lab)
-            lhost[b : b + 1].copy_(loss.detach().reshape(1).float(), non_blocking=True)
-            lready[b].record()
-            if i > 0:
-                lready[1 - b].synchronize()
-                float(lhost[1 - b])
-        lready[(e2e_steps - 1) % 2].synchronize()
-        float(lhost[(e2e_steps - 1) % 2])
+            li = i % (LAG + 1)
+            lhost[li : li + 1].copy_(loss.detach().reshape(1).float(), non_blocking=True)
+            lready[li].record()
+            if i >= LAG:
+                lj = (i - LAG) % (LAG + 1)
+                lready[lj].synchronize()
+                float(lhost[lj])
+        for i in range(max(0, e2e_steps - LAG), e2e_steps):
+            lready[i % (LAG + 1)].synchronize()
+            float(lhost[i % (LAG + 1)])
     else:
         for _ in range(e2e_steps):
             loss = step(xh.to(dev, non_blocking=True), lh.to(dev, non_blocking=True))
