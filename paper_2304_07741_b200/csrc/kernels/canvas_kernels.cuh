@@ -427,6 +427,77 @@ __device__ __forceinline__ void wgrad_small(const CanvasArgs& a) {
   }
 }
 
+// wgrad for few output channels with the 4-pixel functors (F::VEC, S % 4 == 0):
+// no shared-memory staging and one barrier per CTA.  Warp (jg, ps) keeps JW rows
+// j of the J side and all M rows of the M side for its pixel quads in registers:
+// per 128-pixel strip (lane = one quad) it evaluates the M quads once, then per
+// row j one quad of B and 4·M FMAs into lane-private sums acc[j][m].  At the end
+// of the chunk the lane sums are reduced by a fixed xor-shuffle tree, the WP
+// pixel streams in order through shared memory (deterministic).  Strips of one
+// stream are ps, ps + WP, ... so the streams of a CTA read adjacent lines.
+// grid = (ceil(J / (WJ·JW)), 1, chunks).
+template <class F>
+__device__ __forceinline__ void wgrad_small_v(const CanvasArgs& a) {
+  constexpr int M = F::M, JW = F::JW, WJ = F::WJ, WP = 8 / WJ;
+  static_assert(WJ * WP == 8, "8 warps = j groups x pixel streams");
+  __shared__ float red[WP > 1 ? WP : 1][WJ][JW * M];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jg = warp % WJ, ps = warp / WJ;
+  const int jb = (blockIdx.x * WJ + jg) * JW;  // first row of this warp
+  const long long T = a.n * (long long)F::S;
+  const long long tbeg = (long long)blockIdx.z * F::TCHUNK;
+  const long long tend = tbeg + F::TCHUNK < T ? tbeg + F::TCHUNK : T;
+  typename F::A4R ra[M];
+  typename F::B4R rb[JW];
+#pragma unroll
+  for (int m = 0; m < M; ++m) ra[m] = F::A4row(a, m);
+#pragma unroll
+  for (int j = 0; j < JW; ++j) rb[j] = F::B4row(a, jb + j < F::J ? jb + j : F::J - 1);
+  float acc[JW][M];
+#pragma unroll
+  for (int j = 0; j < JW; ++j)
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[j][m] = 0.f;
+  for (long long t = tbeg + 128 * ps + 4 * lane; t < tend; t += 128 * WP) {
+    const long long n = t / F::S;
+    const int s = (int)(t - n * F::S);
+    float av[M][4];
+#pragma unroll
+    for (int m = 0; m < M; ++m) F::A4k(a, ra[m], n, s, av[m]);
+#pragma unroll
+    for (int j = 0; j < JW; ++j) {
+      float bv[4];
+      F::B4k(a, rb[j], n, s, bv);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        float v = acc[j][m];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v = fmaf(av[m][e], bv[e], v);
+        acc[j][m] = v;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < JW; ++j)
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      float v = acc[j][m];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (((j * M + m) & 31) == lane) red[WP > 1 ? ps : 0][jg][j * M + m] = v;
+    }
+  __syncthreads();
+  float* P = F::partials(a) + (long long)blockIdx.z * M * F::J;
+  for (int o = threadIdx.x; o < WJ * JW * M; o += blockDim.x) {
+    const int g = o / (JW * M), r = o - g * (JW * M);
+    const int j = (blockIdx.x * WJ + g) * JW + r / M, m = r % M;
+    float v = 0.f;
+#pragma unroll
+    for (int p = 0; p < WP; ++p) v += red[p][g][r];
+    if (j < F::J) P[(long long)m * F::J + j] = v;
+  }
+}
+
 // F::TJ > 0: partials are [M][TJ] and dW is written transposed ([TJ][M]).
 template <class F>
 __device__ __forceinline__ int reduce_out_index(const int idx) {

@@ -60,6 +60,9 @@ GEMM_TILE = 64
 SLOT_GUARD = 16384  # bytes of guard zone on each side of every saved / workspace tensor (canvas_runtime.cpp kGuard)
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
+FC_SMALL_W4 = os.environ.get("CANVAS_FC_SMALL_W4", "0") == "1"  # per-pixel small FC: 16 B weight rows (measured slower: 0.080 vs 0.070 ms)
+FC_SMALL_UNROLL = int(os.environ.get("CANVAS_FC_SMALL_UNROLL", "0"))  # per-pixel small FC input-loop unroll (0: Fn.loop default)
+WGRAD_SMALL_V = os.environ.get("CANVAS_WGRAD_SMALL_V", "1") == "1"  # register-blocked quad wgrad for M <= 16
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
 INLINE_SMALL_DGRAD = os.environ.get("CANVAS_INLINE_SMALL_DGRAD", "1") == "1"  # few-output FC dgrad inlined into the gradient sum
 SOFTMAX_REG_SPAN = int(os.environ.get("CANVAS_SOFTMAX_REG_SPAN", "64"))  # softmax rows up to this long are held in registers
@@ -1438,7 +1441,7 @@ class Lowerer:
             return None
         return ext[: len(ext) - nsp], ext[len(ext) - nsp:]
 
-    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1, node=None):
+    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1, node=None, align16=False):
         """``inner``: extent of the innermost output dim (per-thread vector width must divide it).
         ``node``: the output node whose elements the threads map to; with H*W >= PLANES_MIN_S
         the launch is plane-major (block-uniform channel plane, threads along pixels)."""
@@ -1497,7 +1500,7 @@ class Lowerer:
             launcher = f'extern "C" __global__ void __launch_bounds__({block}) {name}(const CanvasArgs a) {{ canvas::{tmpl}<{name}_F>(a); }}\n'
             grid = (GridRule(0, chunks, 1), GridRule(Q, 0, 1, min(65535, max(1, PLANES_CTAS // chunks))), GridRule(0, 1, 1))
         k = self.add_kernel(name, functor, launcher)
-        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops, align16=vec16))
+        self.p.launches.append(Launch("kernel", phase, name, k, block, grid, tuple(slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops, align16=vec16 or align16))
 
     # ---- forward
     def fwd_targets(self, v: int) -> list:
@@ -1735,17 +1738,36 @@ class Lowerer:
                 accs = [f.fresh("acc") for _ in range(O)]
                 f.emit("float " + ", ".join(f"{a_} = 0.f" for a_ in accs) + ";")
                 i = f.fresh("i")
-                f.loop(i, K)
-                ch = tuple(f.decompose(i, nv.ch_ext))
-                x = self.val(f, v, ch + sp)
-                for o, a_ in enumerate(accs):
-                    f.emit(f"{a_} = fmaf(__ldg({f.ptr(wslot)} + {o * K} + {i}), {x}, {a_});")
-                f.close()
+                if FC_SMALL_W4 and K % 4 == 0 and K >= 8:
+                    # 4 inputs per step, one 16 B load per output row of W
+                    f.emit("#pragma unroll 2")
+                    f.open(f"for (int {i} = 0; {i} < {K}; {i} += 4)")
+                    xs = []
+                    for e in range(4):
+                        ie = f.ivar(f"{i} + {e}") if e else i
+                        xs.append(self.val(f, v, tuple(f.decompose(ie, nv.ch_ext)) + sp))
+                    for o, a_ in enumerate(accs):
+                        w4 = f.fresh("w")
+                        f.emit(f"const float4 {w4} = __ldg(reinterpret_cast<const float4*>({f.ptr(wslot)} + {o * K} + {i}));" if f.V == 1 else f"float4 {w4} = __ldg(reinterpret_cast<const float4*>({f.ptr(wslot)} + {o * K} + {i}));")
+                        for e, comp in enumerate("xyzw"):
+                            f.emit(f"{a_} = fmaf({w4}.{comp}, {xs[e]}, {a_});")
+                    f.close()
+                else:
+                    if FC_SMALL_UNROLL:
+                        f.emit(f"#pragma unroll {FC_SMALL_UNROLL}")
+                        f.open(f"for (int {i} = 0; {i} < {K}; ++{i})")
+                    else:
+                        f.loop(i, K)
+                    ch = tuple(f.decompose(i, nv.ch_ext))
+                    x = self.val(f, v, ch + sp)
+                    for o, a_ in enumerate(accs):
+                        f.emit(f"{a_} = fmaf(__ldg({f.ptr(wslot)} + {o * K} + {i}), {x}, {a_});")
+                    f.close()
                 for o, a_ in enumerate(accs):
                     for d, b in targets:
                         f.store(d, (str(o),) + sp, a_, b)
 
-            self.launch_pointwise(name, math.prod(nu.sp_ext), body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1)
+            self.launch_pointwise(name, math.prod(nu.sp_ext), body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1, align16=FC_SMALL_W4 and K % 4 == 0 and K >= 8)
             return
         if min(O, K) <= SMALL_FC:
 
@@ -2150,7 +2172,16 @@ class Lowerer:
         # 0.44 ms, im2col / involution (1 load) 0.32 -> 0.39 / 0.064 -> 0.070 ms
         nld_b = sum(ln.count("__ldg") for ln in fb.pre + fb.lines)
         SP = -(-S // 4) * 4 if (use_tc and VEC_PAD and S % 4 and not VEC_NQ and nld_b >= VEC_PAD_MIN_LOADS) else S
-        if small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
+        # register-blocked small wgrad over pixel quads (wgrad_small_v): JW rows of the
+        # J side x all M rows per warp, WJ row groups x 8/WJ pixel streams per CTA
+        small_v = small and WGRAD_SMALL_V and S % 4 == 0
+        if small_v:
+            jw = min(8 if M <= 8 else 2, 1 << max(0, (J - 1).bit_length()))
+            wj = min(8, 1 << max(0, (-(-J // jw) - 1).bit_length()))
+            jblk = -(-J // (jw * wj))
+            z = -(-(4 * SMS) // jblk)  # ~4 CTAs per SM at batch 256
+            tchunk = max(128, -(-(-(-(256 * S) // z)) // 128) * 128)
+        elif small:  # ~8 CTAs per SM at batch 256: chunk = 256*S*jtiles / (8*148), multiple of 64
             jt0 = min(1 << max(0, (256 // M).bit_length() - 1), 1 << max(0, (J - 1).bit_length()), WGRAD_SMALL_JT_MAX)
             tchunk = max(64, -(-(256 * S * -(-J // jt0)) // (8 * SMS * 64)) * 64)
         else:
@@ -2200,6 +2231,12 @@ class Lowerer:
             k = self.add_kernel(name, functor, launcher)
             grid = (GridRule(0, J, 128 * jg), GridRule(0, nct, 1), GridRule(SP, 0, tchunk))
             self.p.launches.append(Launch("kernel", 1, name, k, threads, grid, tuple(fa.local_slots), BETA_NONE, smem=smem, what="tc " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=bool(vb4) and self._op_vec16))
+        elif small_v and vb4 and not nq:
+            functor = functor[: functor.rindex("};")] + f"  static constexpr int JW = {jw}, WJ = {wj};\n}};\n"
+            launcher = f'extern "C" __global__ void __launch_bounds__(256, 2) {name}(const CanvasArgs a) {{ canvas::wgrad_small_v<{name}_F>(a); }}\n'
+            k = self.add_kernel(name, functor, launcher)
+            grid = (GridRule(0, J, jw * wj), GridRule(0, 1, 1), GridRule(S, 0, tchunk))
+            self.p.launches.append(Launch("kernel", 1, name, k, 256, grid, tuple(fa.local_slots), BETA_NONE, what="small " + what, bytes_per_image=nbytes, flops_per_image=flops, align16=self._op_vec16))
         elif small:
             jt = min(1 << max(0, (256 // M).bit_length() - 1), WGRAD_SMALL_JT_MAX)
             jt = min(jt, 1 << (J - 1).bit_length()) if J > 1 else 1

@@ -128,6 +128,8 @@ void gemm_wgrad(const CanvasArgs& a) {
 
 template <class F>
 void wgrad_small(const CanvasArgs& a) { gemm_wgrad<F>(a); }
+template <class F>
+void wgrad_small_v(const CanvasArgs& a) { gemm_wgrad<F>(a); }
 
 template <class F, int SL>
 void softmax_rows(const CanvasArgs& a) {
