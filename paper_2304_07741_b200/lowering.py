@@ -61,7 +61,8 @@ SLOT_GUARD = 16384  # bytes of guard zone on each side of every saved / workspac
 MAX_BATCH = 1024  # images per call; bounds the 32-bit offset arithmetic (canvas_plan_create checks)
 REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times per consumer element
 FC_SMALL_W4 = os.environ.get("CANVAS_FC_SMALL_W4", "0") == "1"  # per-pixel small FC: 16 B weight rows (measured slower: 0.080 vs 0.070 ms)
-FC_SMALL_UNROLL = int(os.environ.get("CANVAS_FC_SMALL_UNROLL", "0"))  # per-pixel small FC input-loop unroll (0: Fn.loop default)
+FC_SMALL_UNROLL = int(os.environ.get("CANVAS_FC_SMALL_UNROLL", "16"))  # per-pixel small FC input-loop unroll (0: Fn.loop default; 16: 0.070 -> 0.068 ms scalar, needed by the quads)
+FC_SMALL_VEC_FILL = int(os.environ.get("CANVAS_FC_SMALL_VEC_FILL", "1024"))  # per-pixel small FC: quads when batch-256 quads >= SMS x this (fc(G) 4x64 at 56^2: 0.070 -> 0.056 ms with unroll 16; at 28^2 quads are slower, 0.081 vs 0.047)
 WGRAD_SMALL_V = os.environ.get("CANVAS_WGRAD_SMALL_V", "1") == "1"  # register-blocked quad wgrad for M <= 16
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
 INLINE_SMALL_DGRAD = os.environ.get("CANVAS_INLINE_SMALL_DGRAD", "1") == "1"  # few-output FC dgrad inlined into the gradient sum
@@ -1441,7 +1442,7 @@ class Lowerer:
             return None
         return ext[: len(ext) - nsp], ext[len(ext) - nsp:]
 
-    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1, node=None, align16=False):
+    def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1, node=None, align16=False, vec_fill=2048):
         """``inner``: extent of the innermost output dim (per-thread vector width must divide it).
         ``node``: the output node whose elements the threads map to; with H*W >= PLANES_MIN_S
         the launch is plane-major (block-uniform channel plane, threads along pixels)."""
@@ -1462,7 +1463,7 @@ class Lowerer:
         # (and enough quads to fill the GPU at the bench batch: per-pixel kernels with
         # a long inner loop — few-output FCs, their adjoints — keep one element per
         # thread at 14x14 and below, measured 45 vs 78 us per launch)
-        if VEC_POINTWISE and (per_image if planes is None else math.prod(planes[1])) % 4 == 0 and per_image * 256 // 4 >= SMS * 2048:
+        if VEC_POINTWISE and (per_image if planes is None else math.prod(planes[1])) % 4 == 0 and per_image * 256 // 4 >= SMS * vec_fill:
             try:
                 vec = self.functor_pointwise(name, per_image, body_fn, planes, V=4)
                 # gathers mostly at sub-16 B shifts (col2im over a 9C gradient): the
@@ -1767,7 +1768,7 @@ class Lowerer:
                     for d, b in targets:
                         f.store(d, (str(o),) + sp, a_, b)
 
-            self.launch_pointwise(name, math.prod(nu.sp_ext), body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1, align16=FC_SMALL_W4 and K % 4 == 0 and K >= 8)
+            self.launch_pointwise(name, math.prod(nu.sp_ext), body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1, align16=FC_SMALL_W4 and K % 4 == 0 and K >= 8, vec_fill=FC_SMALL_VEC_FILL)
             return
         if min(O, K) <= SMALL_FC:
 
