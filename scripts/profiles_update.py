@@ -21,6 +21,9 @@ sys.path.insert(0, os.path.join(ROOT, "scripts"))
 from ncu_summary import summary  # noqa: E402
 
 
+TRAFFIC_KEY = os.environ.get("TRAFFIC_KEY", "seed7_k1|resnet18|64x64@56x56/s1|b256")
+
+
 def main():
     tag, rep, launches = sys.argv[1:4]
     bench = sys.argv[4] if len(sys.argv) > 4 else None
@@ -40,7 +43,10 @@ def main():
         rd = float(d.get("dram__bytes_read.sum", "0 byte").split()[0]) * _unit(d.get("dram__bytes_read.sum", "0 byte"))
         wr = float(d.get("dram__bytes_write.sum", "0 byte").split()[0]) * _unit(d.get("dram__bytes_write.sum", "0 byte"))
         inst = d.get("Executed Instructions", "0 inst").split()[0].replace(",", "")
-        traffic.setdefault("seed7_k1", {})[k.split("_", 1)[1]] = {"batch": 256, "dram_bytes": int(rd + wr), "warp_instructions": int(float(inst)), "source": f"profiles/{tag}_ncu_full.json"}
+        # keyed by the workload that produced the counters (bench.traffic_key): the
+        # capture is the ResNet-18 layer1 target of config 2 (seed-7 #1, 64x64 @ 56x56, b256)
+        traffic.setdefault(TRAFFIC_KEY, {})[k.split("_", 1)[1]] = {"batch": 256, "dram_bytes": int(rd + wr), "warp_instructions": int(float(inst)), "source": f"profiles/{tag}_ncu_full.json"}
+    traffic.pop("seed7_k1", None)  # pre-workload-key format
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     rows = list(csv.reader(open(launches)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)

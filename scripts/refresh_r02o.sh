@@ -1,4 +1,4 @@
-# Round-2 refresh: GPU tests, bench (+ reference arm), configs 3/5, launch list, ncu --set full of the layer1 Canvas kernels
+# Round-2 refresh (r02o): GPU tests, bench (+ reference arm), configs 3/5, launch list, ncu --set full of the layer1 Canvas kernels
 set -x
 mkdir -p gpurun_out/keep
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/keep/gpu_tests.log 2>&1; tail -3 gpurun_out/keep/gpu_tests.log
