@@ -63,6 +63,7 @@ REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times p
 FC_SMALL_W4 = os.environ.get("CANVAS_FC_SMALL_W4", "0") == "1"  # per-pixel small FC: 16 B weight rows (measured slower: 0.080 vs 0.070 ms)
 FC_SMALL_UNROLL = int(os.environ.get("CANVAS_FC_SMALL_UNROLL", "16"))  # per-pixel small FC input-loop unroll (0: Fn.loop default; 16: 0.070 -> 0.068 ms scalar, needed by the quads)
 FC_SMALL_VEC_FILL = int(os.environ.get("CANVAS_FC_SMALL_VEC_FILL", "1024"))  # per-pixel small FC: quads when batch-256 quads >= SMS x this (fc(G) 4x64 at 56^2: 0.070 -> 0.056 ms with unroll 16; at 28^2 quads are slower, 0.081 vs 0.047)
+LOADS_FIRST = os.environ.get("CANVAS_LOADS_FIRST", "0") == "1"  # pointwise bodies: gathers hoisted above the arithmetic
 WGRAD_SMALL_V = os.environ.get("CANVAS_WGRAD_SMALL_V", "1") == "1"  # register-blocked quad wgrad for M <= 16
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
 INLINE_SMALL_DGRAD = os.environ.get("CANVAS_INLINE_SMALL_DGRAD", "1") == "1"  # few-output FC dgrad inlined into the gradient sum
@@ -1427,9 +1428,28 @@ class Lowerer:
             Q, S = math.prod(planes[0]), math.prod(planes[1])
             src = [f"struct {name}_F {{", f"  static constexpr int Q = {Q}, S = {S};", f"  static __device__ __forceinline__ void {fn}(const CanvasArgs& a, const long long n, const int q, const int s) {{", f"    const int r = q * {S} + s;"]
         src += ["    " + s for s in f.pre]
-        src += f.lines
+        src += self.loads_first(f) if LOADS_FIRST else f.lines
         src += ["  }", "};"]
         return "\n".join(src) + "\n", f.local_slots
+
+    @staticmethod
+    def loads_first(f: Fn) -> list:
+        """Straight-line bodies (no loops / braces): index math and gathers hoisted
+        above the float arithmetic, in order, wherever their operands allow — so
+        every gather of the element is issued before the first one is consumed."""
+        lines, tags = f.lines, f.ltags
+        if any("{" in ln or "}" in ln or ln.lstrip().startswith("#") for ln in lines):
+            return lines
+        early, late, late_names = [], [], set()
+        for ln, t in zip(lines, tags):
+            m = re.match(r"\s*(?:const )?(?:int|float|float4|float\*|const float\*)\s*(?:const )?(\w+) = (.*);$", ln)
+            if m and t in "il" and not (set(_IDENT.findall(m.group(2))) & late_names):
+                early.append(ln)
+                continue
+            late.append(ln)
+            if m:
+                late_names.add(m.group(1))
+        return early + late
 
     @staticmethod
     def plane_split(ext, sp_ext, per_image):
