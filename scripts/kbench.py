@@ -81,6 +81,45 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     layer_ms = e0.elapsed_time(e1) / a.iters
+    # the same fwd+bwd captured once as a CUDA graph and replayed (no host launch
+    # overhead: the figure that matters at small batch, e.g. config 1 at N = 8)
+    g = torch.cuda.CUDAGraph()
+    s_cap = torch.cuda.Stream()
+    s_cap.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s_cap):
+        st_cap = s_cap.cuda_stream
+        dp.forward(x, ws, y, saved, st_cap)
+        dp.backward(x, ws, saved, dy, dx, dws, work, st_cap)
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s_cap):
+            dp.forward(x, ws, y, saved, st_cap)
+            dp.backward(x, ws, saved, dy, dx, dws, work, st_cap)
+    torch.cuda.synchronize()
+    for _ in range(3):
+        g.replay()
+    e0.record()
+    for _ in range(a.iters * 4):
+        g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    graph_ms = e0.elapsed_time(e1) / (a.iters * 4)
+    # context: cuDNN nn.Conv2d of the replaced shape, fwd + dgrad + wgrad, TF32 off / on
+    ctx = {}
+    conv = torch.nn.Conv2d(a.cin, a.cout, a.k, a.stride, padding=a.k // 2, bias=False).to(dev)
+    xc = x.clone().requires_grad_(True)
+    torch.backends.cudnn.benchmark = True
+    for tf32 in (False, True):
+        torch.backends.cudnn.allow_tf32 = tf32
+        for _ in range(3):
+            conv(xc).backward(dy)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(a.iters):
+            conv(xc).backward(dy)
+        e1.record()
+        torch.cuda.synchronize()
+        ctx["cudnn_conv_tf32" if tf32 else "cudnn_conv_fp32"] = round(e0.elapsed_time(e1) / a.iters, 4)
+    torch.backends.cudnn.allow_tf32 = False
     rows = []
     for i, L in enumerate(plan.launches):
         if L.kind != "kernel":
@@ -101,12 +140,13 @@ def main():
         tf = L.flops_per_image * n / (ms * 1e-3) / 1e12 if L.flops_per_image else 0.0
         rows.append({"name": L.name, "what": L.what, "ms": round(ms, 4), "GBps": round(gbs, 1), "TFLOPs": round(tf, 2), "hbm_frac": round(gbs / peaks["hbm_gbs"], 3), "tf32_frac": round(tf / tf32_peak, 4)})
     tot = sum(r["ms"] for r in rows)
-    print(f"layer {a.kernel} {a.cin}->{a.cout} {a.hw}^2 s{a.stride} batch {n}: fwd+bwd {layer_ms:.3f} ms (sum of launches {tot:.3f} ms)")
+    print(f"layer {a.kernel} {a.cin}->{a.cout} {a.hw}^2 s{a.stride} batch {n}: fwd+bwd {layer_ms:.3f} ms (sum of launches {tot:.3f} ms; CUDA-graph replay {graph_ms:.3f} ms)")
+    print(f"  context: cuDNN nn.Conv2d {a.cin}->{a.cout} k{a.k} s{a.stride} fwd+bwd: fp32 {ctx['cudnn_conv_fp32']:.3f} ms, TF32 {ctx['cudnn_conv_tf32']:.3f} ms")
     for r in rows:
         print(f"  {r['ms']:8.3f} ms {100 * r['ms'] / tot:5.1f}%  {r['GBps']:8.1f} GB/s  {r['TFLOPs']:7.2f} TF/s  {r['name']:28s} {r['what']}")
     if a.json:
         with open(a.json, "w") as f:
-            json.dump({"args": vars(a), "layer_ms": layer_ms, "rows": rows}, f, indent=1)
+            json.dump({"args": vars(a), "layer_ms": layer_ms, "graph_ms": graph_ms, "context": ctx, "rows": rows}, f, indent=1)
 
 
 if __name__ == "__main__":
