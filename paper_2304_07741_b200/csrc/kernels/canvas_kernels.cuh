@@ -89,6 +89,33 @@ __device__ __forceinline__ void pointwise(const CanvasArgs& a) {
   }
 }
 
+// KS consecutive lanes per output element (few outputs, long reduction): F::part
+// accumulates lane `part`'s share of the reduction (terms part, part + KS, ...), the
+// KS partial sums are combined by a fixed xor-shuffle tree (deterministic) and the
+// group's first lane stores.  The element loop is block-uniform, so every lane of a
+// warp reaches the shuffles; lanes past the end evaluate a clamped element.
+template <class F, int KS>
+__device__ __forceinline__ void pointwise_ks(const CanvasArgs& a) {
+  static_assert(KS >= 2 && KS <= 32 && (KS & (KS - 1)) == 0, "KS: power of 2 <= 32");
+  const long long total = a.n * F::PER;
+  const int part = threadIdx.x % KS;
+  const long long per_block = blockDim.x / KS;
+  for (long long base = (long long)blockIdx.x * per_block; base < total; base += (long long)gridDim.x * per_block) {
+    const long long i = base + threadIdx.x / KS;
+    const bool ok = i < total;
+    const long long ic = ok ? i : total - 1;
+    const long long n = ic / F::PER;
+    const int r = (int)(ic - n * F::PER);
+    float acc[F::NACC];
+    F::part(a, n, r, part, acc);
+#pragma unroll
+    for (int j = 0; j < F::NACC; ++j)
+#pragma unroll
+      for (int o = KS / 2; o > 0; o >>= 1) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    if (ok && part == 0) F::put(a, n, r, acc);
+  }
+}
+
 // Plane-major variant: blockIdx.y = (image, channel plane) — block-uniform, so the
 // functor's channel index math (flat-channel decomposition, replica/tap
 // indices) runs once per warp on the uniform datapath — and the threads of

@@ -64,6 +64,7 @@ FC_SMALL_W4 = os.environ.get("CANVAS_FC_SMALL_W4", "0") == "1"  # per-pixel smal
 FC_SMALL_UNROLL = int(os.environ.get("CANVAS_FC_SMALL_UNROLL", "16"))  # per-pixel small FC input-loop unroll (0: Fn.loop default; 16: 0.070 -> 0.068 ms scalar, needed by the quads)
 FC_SMALL_VEC_FILL = int(os.environ.get("CANVAS_FC_SMALL_VEC_FILL", "1024"))  # per-pixel small FC: quads when batch-256 quads >= SMS x this (fc(G) 4x64 at 56^2: 0.070 -> 0.056 ms with unroll 16; at 28^2 quads are slower, 0.081 vs 0.047)
 LOADS_FIRST = os.environ.get("CANVAS_LOADS_FIRST", "1") == "1"  # pointwise bodies: gathers hoisted above the arithmetic (grad n1: 0.186 -> 0.165 ms at 14^2, 0.113 -> 0.086 at 7^2, 56^2 unchanged)
+FC_SMALL_KS = os.environ.get("CANVAS_FC_SMALL_KS", "1") == "1"  # per-output small FC with few pixels: K split over lanes
 WGRAD_SMALL_V = os.environ.get("CANVAS_WGRAD_SMALL_V", "1") == "1"  # register-blocked quad wgrad for M <= 16
 WGRAD_SMALL_JT_MAX = 128  # wgrad_small stages (M + JT) x 65 floats: <= 48 KB of static shared memory for M <= 56
 INLINE_SMALL_DGRAD = os.environ.get("CANVAS_INLINE_SMALL_DGRAD", "1") == "1"  # few-output FC dgrad inlined into the gradient sum
@@ -1462,6 +1463,42 @@ class Lowerer:
             return None
         return ext[: len(ext) - nsp], ext[len(ext) - nsp:]
 
+    @staticmethod
+    def ks_split(per_image: int, K: int) -> int:
+        """Lanes per output element for a long per-element reduction (K terms): the largest
+        power of 2 <= 32 keeping the batch-256 thread count within 2 full waves and >= 16
+        terms per lane; 1 = no split."""
+        if not FC_SMALL_KS or K < 64:
+            return 1
+        ks = 1
+        while ks < 32 and per_image * 256 * ks * 2 <= SMS * 2048 * 2 and K // (ks * 2) >= 16:
+            ks *= 2
+        return ks
+
+    def launch_ks(self, name, per_image, part_fn, put_fn, nacc, ks, phase, beta, what, nbytes, flops):
+        """``canvas::pointwise_ks``: KS consecutive lanes per output element; ``part``
+        accumulates the lane's share into acc[0 .. nacc), the template reduces over the KS
+        lanes (fixed xor tree), ``put`` stores from the first lane."""
+        f = Fn(self)
+        f.pre = []
+        f.computing = None
+        part_fn(f)
+        g = Fn(self)
+        g.pre = []
+        g.computing = None
+        g.local_slots = f.local_slots
+        put_fn(g)
+        src = [f"struct {name}_F {{", f"  static constexpr long long PER = {per_image}LL;", f"  static constexpr int NACC = {nacc};",
+               f"  static __device__ __forceinline__ void part(const CanvasArgs& a, const long long n, const int r, const int part, float* acc) {{"]
+        src += ["    " + x for x in f.pre] + f.lines + ["  }"]
+        src += ["  static __device__ __forceinline__ void put(const CanvasArgs& a, const long long n, const int r, const float* acc) {"]
+        src += ["    " + x for x in g.pre] + g.lines + ["  }", "};"]
+        functor = "\n".join(src) + "\n"
+        launcher = f'extern "C" __global__ void __launch_bounds__({POINTWISE_BLOCK}) {name}(const CanvasArgs a) {{ canvas::pointwise_ks<{name}_F, {ks}>(a); }}\n'
+        k = self.add_kernel(name, functor, launcher)
+        grid = (GridRule(per_image * ks, 0, POINTWISE_BLOCK, POINTWISE_CAP), GridRule(0, 1, 1), GridRule(0, 1, 1))
+        self.p.launches.append(Launch("kernel", phase, name, k, POINTWISE_BLOCK, grid, tuple(f.local_slots), beta, what=what, bytes_per_image=nbytes, flops_per_image=flops))
+
     def launch_pointwise(self, name, per_image, body_fn, phase, beta=BETA_NONE, what="", nbytes=0, flops=0, inner=1, node=None, align16=False, vec_fill=2048):
         """``inner``: extent of the innermost output dim (per-thread vector width must divide it).
         ``node``: the output node whose elements the threads map to; with H*W >= PLANES_MIN_S
@@ -1789,6 +1826,33 @@ class Lowerer:
                         f.store(d, (str(o),) + sp, a_, b)
 
             self.launch_pointwise(name, math.prod(nu.sp_ext), body, 0, beta, f"fc_small {O}x{K} -> n{u}", io, flops, inner=nu.ext[-1] if nu.ext else 1, align16=FC_SMALL_W4 and K % 4 == 0 and K >= 8, vec_fill=FC_SMALL_VEC_FILL)
+            return
+        ks = self.ks_split(nu.numel, K) if min(O, K) <= SMALL_FC else 1
+        if ks > 1:
+            # few pixels, long reduction (fc(G) at 14x14 / 7x7: K = 256-512 per output):
+            # KS lanes per output element split the K loop, xor-shuffle reduce
+
+            def part(f, u=u):
+                c = tuple(f.decompose("r", nu.ext))
+                o, sp = c[0], c[1:]
+                acc = f.fresh("acc")
+                f.emit(f"float {acc} = 0.f;")
+                wrow = f.ivar(f"{o}*{K}")
+                i = f.fresh("i")
+                f.emit("#pragma unroll 4")
+                f.open(f"for (int {i} = part; {i} < {K}; {i} += {ks})")
+                ch = tuple(f.decompose(i, nv.ch_ext))
+                x = self.val(f, v, ch + sp)
+                f.emit(f"{acc} = fmaf(__ldg({f.ptr(wslot)} + {wrow} + {i}), {x}, {acc});")
+                f.close()
+                f.emit(f"acc[0] = {acc};")
+
+            def put(f):
+                c = tuple(f.decompose("r", nu.ext))
+                for d, b in targets:
+                    f.store(d, c, "acc[0]", b)
+
+            self.launch_ks(name, nu.numel, part, put, 1, ks, 0, beta, f"fc_small {O}x{K} -> n{u} (K split {ks})", io, flops)
             return
         if min(O, K) <= SMALL_FC:
 

@@ -63,6 +63,20 @@ void pointwise(const CanvasArgs& a) {
     for (int r = 0; r < (int)F::PER; ++r) F::run(a, n, r);
 }
 
+template <class F, int KS>
+void pointwise_ks(const CanvasArgs& a) {
+  for (long long n = 0; n < a.n; ++n)
+    for (int r = 0; r < (int)F::PER; ++r) {
+      float tot[F::NACC] = {};
+      for (int p = 0; p < KS; ++p) {
+        float acc[F::NACC];
+        F::part(a, n, r, p, acc);
+        for (int j = 0; j < F::NACC; ++j) tot[j] += acc[j];
+      }
+      F::put(a, n, r, tot);
+    }
+}
+
 template <class F>
 void pointwise_planes(const CanvasArgs& a) {
   for (long long n = 0; n < a.n; ++n)

@@ -265,3 +265,12 @@ def test_gradient_siblings(name, monkeypatch):
         assert_close(case, *emu_run(case), f"{name} siblings")
     finally:
         executor._plan_cached.cache_clear()
+
+
+@pytest.mark.parametrize("cin,hw", [(64, 8), (128, 7), (256, 5)])
+def test_ksplit_small_fc(cin, hw):
+    """Few pixels, long reduction: fc(G) with its K = C loop split over lanes
+    (canvas::pointwise_ks), the partial sums reduced before the store."""
+    case = reference(zoo.SEED7_K1, cin, cin, hw, hw, n=2)
+    assert any("K split" in L.what for L in case.plan.launches), [L.what for L in case.plan.launches]
+    assert_close(case, *emu_run(case), f"seed7_k1 {cin} {hw}x{hw}")
