@@ -1194,6 +1194,27 @@ __device__ __forceinline__ void tc_gemm_pix(const CanvasArgs& a) {
 // K-major SW128 images by bulk copy, as in tc_gemm_pix.  TMEM: NACC x NT
 // accumulator columns, then STAGES x {A_hi 32, A_lo 32} columns.
 // ---------------------------------------------------------------------------
+template <int V>
+struct IntC {
+  static constexpr int value = V;
+};
+#ifndef CANVAS_TMEMA_UNROLL_K
+#define CANVAS_TMEMA_UNROLL_K 1024
+#endif
+constexpr int kTmemaUnrollK = CANVAS_TMEMA_UNROLL_K;  // full k-block unroll up to this K
+
+// KS consecutive k of k-block kb (share hs) at this thread's pixel
+template <class F, int KS>
+__device__ __forceinline__ void tmema_gather(const CanvasArgs& a, const int kb, const int hs, const long long n, const int s, const bool ok, float* v) {
+#pragma unroll
+  for (int i = 0; i < KS; ++i) {
+    const int k = kb * tc::kBK + hs * KS + i;
+    const int kc = k < F::K ? k : F::K - 1;
+    const float x = F::Bk(a, F::Brow(a, kc), n, s);
+    v[i] = (ok && k < F::K) ? x : 0.f;
+  }
+}
+
 template <class F, int NT, int STAGES, int NACC = 1, int PW = 8>
 __device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
   using namespace tc;
@@ -1238,38 +1259,45 @@ __device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
     const long long n = ok ? t / F::S : 0;
     const int s = ok ? (int)(t - n * F::S) : 0;
     const cv_u32 lane_base = tmem + ((cv_u32)(q * 32) << 16);
-    float hi[16], lo[16], v[KS];
-    auto gather = [&](int kb) {
+    // HC >= 0: the k share is a compile-time constant and the k-block loop is fully
+    // unrolled (F::K <= kTmemaUnrollK), so every k of the producer is a constant and
+    // the functor's row context (channel / tap decomposition, plane offsets) folds
+    // into immediates: per element only the gathers, the combine and the split remain
+    auto produce = [&](auto hc) {
+      constexpr int HC = decltype(hc)::value;
+      constexpr int UF = HC >= 0 ? KB : 1;
+      const int hs = HC >= 0 ? HC : half;
+      float hi[KS], lo[KS], v[KS];
+      tmema_gather<F, KS>(a, 0, hs, n, s, ok, v);
+#pragma unroll UF
+      for (int kb = 0; kb < KB; ++kb) {
+        const int st = kb % STAGES;
 #pragma unroll
-      for (int i = 0; i < KS; ++i) {
-        const int k = kb * kBK + half * KS + i;
-        const int kc = k < F::K ? k : F::K - 1;
-        const float x = F::Bk(a, F::Brow(a, kc), n, s);
-        v[i] = (ok && k < F::K) ? x : 0.f;
+        for (int i = 0; i < KS; ++i) split_tf32(v[i], hi[i], lo[i]);
+        if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
+        fence_after();
+        const cv_u32 acol = lane_base + ACOL + st * 64 + hs * KS;
+        if constexpr (KS >= 16) {
+#pragma unroll
+          for (int j = 0; j < KS; j += 16) {
+            tmem_st16(acol + j, hi + j);
+            tmem_st16(acol + 32 + j, lo + j);
+          }
+        } else {
+          tmem_st8(acol, hi);
+          tmem_st8(acol + 32, lo);
+        }
+        tmem_st_wait();
+        fence_before();
+        mbar_arrive(&full[st]);
+        if (kb + 1 < KB) tmema_gather<F, KS>(a, kb + 1, hs, n, s, ok, v);
       }
     };
-    gather(0);
-    for (int kb = 0; kb < KB; ++kb) {
-      const int st = kb % STAGES;
-#pragma unroll
-      for (int i = 0; i < KS; ++i) split_tf32(v[i], hi[i], lo[i]);
-      if (kb >= STAGES) mbar_wait(&empty[st], ((kb / STAGES) & 1) ^ 1);
-      fence_after();
-      const cv_u32 acol = lane_base + ACOL + st * 64 + half * KS;
-      if constexpr (KS >= 16) {
-#pragma unroll
-        for (int j = 0; j < KS; j += 16) {
-          tmem_st16(acol + j, hi + j);
-          tmem_st16(acol + 32 + j, lo + j);
-        }
-      } else {
-        tmem_st8(acol, hi);
-        tmem_st8(acol + 32, lo);
-      }
-      tmem_st_wait();
-      fence_before();
-      mbar_arrive(&full[st]);
-      if (kb + 1 < KB) gather(kb + 1);
+    if constexpr (F::K <= kTmemaUnrollK && PW == 8) {
+      if (half == 0) produce(IntC<0>{});
+      else produce(IntC<1>{});
+    } else {
+      produce(IntC<-1>{});
     }
     // epilogue: TMEM lane quadrant = q, column half = warp / 4
     mbar_wait(done, 0);

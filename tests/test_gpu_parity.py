@@ -192,7 +192,7 @@ def test_image_quad_wgrad(name, n, monkeypatch):
     assert_close(case, *run_gpu(case), f"{name} NQ n{n}")
 
 
-@pytest.mark.parametrize("name,cin,hw", [("seed7_k1", 64, 16), ("im2col", 128, 8), ("seed7_k1", 128, 7)])
+@pytest.mark.parametrize("name,cin,hw", [("seed7_k1", 64, 16), ("im2col", 128, 8), ("seed7_k1", 128, 7), ("im2col", 64, 12), ("seed7_k1", 96, 9)])
 def test_fc_forward_tmem_a(name, cin, hw, monkeypatch):
     """FC forward with the computed operand staged in tensor memory (tcgen05.mma
     with A from TMEM, producers writing it with tcgen05.st; CANVAS_TMEMA=1, off by
