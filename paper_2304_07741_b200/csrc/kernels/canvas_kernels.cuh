@@ -1198,11 +1198,6 @@ template <int V>
 struct IntC {
   static constexpr int value = V;
 };
-#ifndef CANVAS_TMEMA_UNROLL_K
-#define CANVAS_TMEMA_UNROLL_K 1024
-#endif
-constexpr int kTmemaUnrollK = CANVAS_TMEMA_UNROLL_K;  // full k-block unroll up to this K
-
 // KS consecutive k of k-block kb (share hs) at this thread's pixel
 template <class F, int KS>
 __device__ __forceinline__ void tmema_gather(const CanvasArgs& a, const int kb, const int hs, const long long n, const int s, const bool ok, float* v) {
@@ -1215,7 +1210,7 @@ __device__ __forceinline__ void tmema_gather(const CanvasArgs& a, const int kb, 
   }
 }
 
-template <class F, int NT, int STAGES, int NACC = 1, int PW = 8>
+template <class F, int NT, int STAGES, int NACC = 1, int PW = 8, bool UNROLL = false>
 __device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
   using namespace tc;
   static_assert(PW == 4 || PW == 8 || PW == 16, "4 lane quadrants x (1, 2 or 4) k shares");
@@ -1260,7 +1255,7 @@ __device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
     const int s = ok ? (int)(t - n * F::S) : 0;
     const cv_u32 lane_base = tmem + ((cv_u32)(q * 32) << 16);
     // HC >= 0: the k share is a compile-time constant and the k-block loop is fully
-    // unrolled (F::K <= kTmemaUnrollK), so every k of the producer is a constant and
+    // unrolled (UNROLL: the lowering's K <= TMEMA_UNROLL_MAX), so every k of the producer is a constant and
     // the functor's row context (channel / tap decomposition, plane offsets) folds
     // into immediates: per element only the gathers, the combine and the split remain
     auto produce = [&](auto hc) {
@@ -1293,7 +1288,7 @@ __device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
         if (kb + 1 < KB) tmema_gather<F, KS>(a, kb + 1, hs, n, s, ok, v);
       }
     };
-    if constexpr (F::K <= kTmemaUnrollK && PW == 8) {
+    if constexpr (UNROLL && PW == 8) {
       if (half == 0) produce(IntC<0>{});
       else produce(IntC<1>{});
     } else {

@@ -83,7 +83,13 @@ VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launche
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
 TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares)
-TC_TMEMA = os.environ.get("CANVAS_TMEMA", "0") == "1"  # FC forward: computed operand staged in TMEM (tcgen05.mma A from TMEM; parity-green, measured 0.79 vs 0.68 ms on layer1: off)
+TC_TMEMA = os.environ.get("CANVAS_TMEMA", "auto")  # FC forward with the computed operand staged in TMEM (tcgen05.mma A from TMEM): "auto" = when its k loop unrolls fully (K <= TMEMA_UNROLL_MAX), "1" always, "0" never
+TMEMA_UNROLL_MAX = int(os.environ.get("CANVAS_TMEMA_UNROLL_MAX", "1024"))  # fully unrolled TMEM-A producers up to this K (layer1 FC forward 0.656 -> 0.390 ms; without the unroll TMEM-A measured 0.79 ms)
+
+
+def tmema_wanted(K: int) -> bool:
+    mode = str(TC_TMEMA)
+    return mode in ("1", "True") or (mode == "auto" and K <= TMEMA_UNROLL_MAX)
 VEC_PAD = os.environ.get("CANVAS_VEC_PAD", "1") == "1"  # S % 4 != 0: wgrad producers on quads of a padded pixel range
 VEC_PAD_MIN_LOADS = int(os.environ.get("CANVAS_VEC_PAD_MIN_LOADS", "2"))
 VEC_PAD_FWD = os.environ.get("CANVAS_VEC_PAD_FWD", "0") == "1"  # same for the FC forward / dgrad quads (7x7 fwd fc: 0.524 vs 0.428 ms scalar: off)
@@ -2120,7 +2126,7 @@ class Lowerer:
         nacc_p = 1
         while nacc_p < 4 and K > TC_ACC_K * nacc_p:
             nacc_p *= 2
-        pix_path = tc and not epi and not TC_TMEMA and TC_A_MN == "true" and not (TC_PERSIST and K < 4 * tc_tile(M, min(TC_NTMAX, 512 // nacc_p))[0])
+        pix_path = tc and not epi and not tmema_wanted(K) and TC_A_MN == "true" and not (TC_PERSIST and K < 4 * tc_tile(M, min(TC_NTMAX, 512 // nacc_p))[0])
         SP = -(-S // 4) * 4 if (pix_path and VEC_PAD_FWD and S % 4) else S
         vec = self.vec_operand("B4", bfn, "k", S, fa.local_slots, pad=SP != S)
         if not vec:
@@ -2192,14 +2198,14 @@ class Lowerer:
                 return False
             # computed operand staged in tensor memory (A from TMEM): lane = pixel, no
             # smem stores; needs accumulators + 3 A stages (64 columns each) in TMEM
-            if TC_TMEMA and not do_save and nacc * nt + 64 * 3 <= 512:
+            if tmema_wanted(K) and not do_save and nacc * nt + 64 * 3 <= 512:
                 tstages = 3
                 tcols = nacc * nt + 64 * tstages
                 tpair = tcols <= 256
                 tsmem = tstages * 2 * nt * 128 + (2 * tstages + 1) * 8 + 16 + 1024
                 tpw = TC_TMEMA_PW
                 tthreads = (tpw + 2) * 32
-                launcher = f'extern "C" __global__ void __launch_bounds__({tthreads}, {2 if tpair and tpw <= 8 else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_tmema<{name}_F, {nt}, {tstages}, {nacc}, {tpw}>(a); }}\n'
+                launcher = f'extern "C" __global__ void __launch_bounds__({tthreads}, {2 if tpair and tpw <= 8 else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_tmema<{name}_F, {nt}, {tstages}, {nacc}, {tpw}, {'true' if K <= TMEMA_UNROLL_MAX and tpw == 8 else 'false'}>(a); }}\n'
                 k = self.add_kernel(name, functor, launcher)
                 pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
                 total = nct * kb * nt * 32

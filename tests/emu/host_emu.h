@@ -288,7 +288,7 @@ template <class F, int NT, int STAGES, bool PACKED, bool A_MN, int PW = 8, int N
 void tc_gemm_pix(const CanvasArgs& a) { gemm_nk_tc<F>(a); }
 template <class F, int NT>
 void tc_pack_b(const CanvasArgs&) {}
-template <class F, int NT, int STAGES, int NACC = 1, int PW = 8>
+template <class F, int NT, int STAGES, int NACC = 1, int PW = 8, bool UNROLL = false>
 void tc_gemm_pix_tmema(const CanvasArgs& a) { gemm_nk<F>(a); }
 template <class F, int NT, int STAGES, int PW, int EW>
 void tc_gemm_pix_persistent(const CanvasArgs& a) { gemm_nk_tc<F>(a); }

@@ -220,6 +220,8 @@ def test_padded_quad_wgrad(name, cin, hw, stride, n, fwd, monkeypatch):
 
     monkeypatch.setattr(lowering, "VEC_PAD_MIN_LOADS", 1)
     monkeypatch.setattr(lowering, "VEC_PAD_FWD", fwd)
+    if fwd:
+        monkeypatch.setattr(lowering, "TC_TMEMA", "0")  # the padded quad smem forward, not TMEM-A
     executor._plan_cached.cache_clear()
     try:
         case = reference(zoo.ALL[name], cin, cin, hw, hw, stride=stride, n=n)

@@ -71,6 +71,7 @@ def test_padded_quad_wgrad(name, hw, stride, n, fwd, monkeypatch):
 
     monkeypatch.setattr(lowering, "VEC_PAD_MIN_LOADS", 1)  # every kernel, not only gather-bound ones
     monkeypatch.setattr(lowering, "VEC_PAD_FWD", fwd)
+    monkeypatch.setattr(lowering, "TC_TMEMA", "0")  # the quad smem forward (TMEM-A takes K <= 1024 by default)
     executor._plan_cached.cache_clear()
     try:
         case = reference(zoo.ALL[name], 32, 32, hw, hw, stride=stride, n=n)
