@@ -774,6 +774,10 @@ struct TmemCols {
   static constexpr int value = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 };
 
+#ifndef CANVAS_WGRAD_STACK
+#define CANVAS_WGRAD_STACK 1
+#endif
+constexpr bool WGRAD_STACK = CANVAS_WGRAD_STACK;  // stacked-N hi.hi + hi.lo wgrad MMA (wgrad_stack)
 constexpr int kProducerWarps = 8;
 constexpr int kThreads = (kProducerWarps + 2) * 32;  // + MMA warp + bulk-copy warp
 constexpr int kBM = 128;  // MMA rows per tile
@@ -806,10 +810,19 @@ struct SmemW {
 
 // wgrad MMA issuer: per k-block, JG row tiles x 4 K=8 steps x 3 MMAs, tile g
 // accumulating into TMEM columns [g*NT, (g+1)*NT)
+// wgrad_stack<NT>(): with 2·NT <= 256 the hi.hi and hi.lo products are ONE MMA of
+// N = 2·NT over the contiguous [B_hi; B_lo] rows (A_hi read from shared memory once
+// instead of twice), accumulating into columns [0, NT) and [NT, 2·NT) of the tile's
+// region; lo.hi adds into [0, NT); the epilogue sums the two halves
+template <int NT>
+__host__ __device__ constexpr bool wgrad_stack() { return WGRAD_STACK && 2 * NT <= 256; }
+
 template <int NT, int JG, int STAGES>
 __device__ __forceinline__ void mma_loop_w(uint8_t* smem, cv_u64* full, cv_u64* empty, cv_u64* done, cv_u32 tmem, int KB) {
   using L = SmemW<NT, JG, STAGES>;
+  constexpr bool STACK = wgrad_stack<NT>();
   constexpr cv_u32 idesc = idesc_tf32(NT, false);
+  constexpr cv_u32 idesc2 = idesc_tf32(STACK ? 2 * NT : NT, false);
   for (int kb = 0; kb < KB; ++kb) {
     const int st = kb % STAGES;
     mbar_wait(&full[st], (kb / STAGES) & 1);
@@ -821,13 +834,18 @@ __device__ __forceinline__ void mma_loop_w(uint8_t* smem, cv_u64* full, cv_u64* 
     for (int g = 0; g < JG; ++g) {
       const cv_u32 a_hi = base + g * L::A_TILE;
       const cv_u32 a_lo = a_hi + L::A_BYTES;
-      const cv_u32 d = tmem + g * NT;
+      const cv_u32 d = tmem + g * (STACK ? 2 * NT : NT);
 #pragma unroll
       for (int kk = 0; kk < kBK / 8; ++kk) {
         const cv_u32 o = kk * 32;
-        mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_hi + o), idesc, !(kb == 0 && kk == 0));
-        mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_lo + o), idesc, 1);
-        mma_tf32(d, desc_k_sw128(a_lo + o), desc_k_sw128(b_hi + o), idesc, 1);
+        if constexpr (STACK) {
+          mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_hi + o), idesc2, !(kb == 0 && kk == 0));
+          mma_tf32(d, desc_k_sw128(a_lo + o), desc_k_sw128(b_hi + o), idesc, 1);
+        } else {
+          mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_hi + o), idesc, !(kb == 0 && kk == 0));
+          mma_tf32(d, desc_k_sw128(a_hi + o), desc_k_sw128(b_lo + o), idesc, 1);
+          mma_tf32(d, desc_k_sw128(a_lo + o), desc_k_sw128(b_hi + o), idesc, 1);
+        }
       }
     }
     commit(&empty[st]);
@@ -1759,7 +1777,8 @@ template <class F, int NT, int STAGES, int PW = tc::kProducerWarps, int JG = 1>
 __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
   using namespace tc;
   using L = SmemW<NT, JG, STAGES>;
-  constexpr int NCOLS = TmemCols<NT * JG>::value;
+  constexpr bool STACK = wgrad_stack<NT>();
+  constexpr int NCOLS = TmemCols<NT * JG * (STACK ? 2 : 1)>::value;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem(smem_raw);
   cv_u64* full = (cv_u64*)(smem + L::BAR_OFF);
@@ -2074,7 +2093,13 @@ __device__ __forceinline__ void tc_gemm_wgrad(const CanvasArgs& a) {
       const int g = u / CH, cc = (u - g * CH) * 16;
       const int jj = j0 + g * kBM + q * 32 + lane;
       float v[16];
-      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + g * NT + cc, v);
+      tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + g * (STACK ? 2 * NT : NT) + cc, v);
+      if constexpr (STACK) {
+        float u[16];
+        tmem_ld16(tmem + ((cv_u32)(q * 32) << 16) + g * 2 * NT + NT + cc, u);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += u[j];
+      }
       if (jj < F::J) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
