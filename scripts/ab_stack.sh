@@ -1,6 +1,6 @@
 # A/B: stacked-N wgrad MMA (hi.hi + hi.lo as one N = 2 NT MMA) vs 3 MMAs, then the GPU suite
 mkdir -p gpurun_out/ab8
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_pinning.py -q -p no:cacheprovider -x 2>&1 | tail -2
+CANVAS_WGRAD_STACK=1 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_pinning.py -q -p no:cacheprovider -x 2>&1 | tail -2
 for i in 1 2; do
 for v in 0 1; do
   for hw in 56 28; do
