@@ -84,6 +84,7 @@ VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B 
 VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
 TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares)
 TC_TMEMA = os.environ.get("CANVAS_TMEMA", "auto")  # FC forward with the computed operand staged in TMEM (tcgen05.mma A from TMEM): "auto" = when its k loop unrolls fully (K <= TMEMA_UNROLL_MAX), "1" always, "0" never
+TMEMA_STAGES = int(os.environ.get("CANVAS_TMEMA_STAGES", "0"))  # TMEM-A operand stages (0: 3, or 2 when that pairs CTAs)
 TMEMA_UNROLL_MAX = int(os.environ.get("CANVAS_TMEMA_UNROLL_MAX", "1024"))  # fully unrolled TMEM-A producers up to this K (layer1 FC forward 0.656 -> 0.390 ms; without the unroll TMEM-A measured 0.79 ms; at 2304: layer2 K = 1152 0.40 -> 0.54 ms — NT = 128 + 3 A stages > 256 TMEM columns, one CTA per SM — layer3 0.26 -> 0.25)
 
 
@@ -2199,7 +2200,8 @@ class Lowerer:
             # computed operand staged in tensor memory (A from TMEM): lane = pixel, no
             # smem stores; needs accumulators + 3 A stages (64 columns each) in TMEM
             if tmema_wanted(K) and not do_save and nacc * nt + 64 * 3 <= 512:
-                tstages = 3
+                # 3 A stages; 2 when that lets two CTAs share the SM's 512 TMEM columns
+                tstages = TMEMA_STAGES or (3 if nacc * nt + 64 * 3 <= 256 or nacc * nt + 64 * 2 > 256 else 2)
                 tcols = nacc * nt + 64 * tstages
                 tpair = tcols <= 256
                 tsmem = tstages * 2 * nt * 128 + (2 * tstages + 1) * 8 + 16 + 1024
