@@ -775,7 +775,7 @@ struct TmemCols {
 };
 
 #ifndef CANVAS_WGRAD_STACK
-#define CANVAS_WGRAD_STACK 0
+#define CANVAS_WGRAD_STACK 1
 #endif
 constexpr bool WGRAD_STACK = CANVAS_WGRAD_STACK;  // stacked-N hi.hi + hi.lo wgrad MMA (wgrad_stack)
 constexpr int kProducerWarps = 8;

@@ -2733,7 +2733,7 @@ class Lowerer:
         fix = lambda s: p.slot_ws(-1 - s) if s < 0 else s  # noqa: E731
         for L in p.launches:
             L.slots = tuple(fix(s) for s in L.slots)
-        header = ("#define CANVAS_RAW_HI 1\n" if os.environ.get("CANVAS_RAW_HI") == "1" else "") + ("#define CANVAS_WGRAD_STACK 1\n" if os.environ.get("CANVAS_WGRAD_STACK") == "1" else "") + '#include "canvas_kernels.cuh"\n'
+        header = ("#define CANVAS_RAW_HI 1\n" if os.environ.get("CANVAS_RAW_HI") == "1" else "") + ("#define CANVAS_WGRAD_STACK 0\n" if os.environ.get("CANVAS_WGRAD_STACK") == "0" else "") + '#include "canvas_kernels.cuh"\n'
         p.source = header + "\n".join(self.kernels)
         del nsv
 
