@@ -50,6 +50,7 @@ def main():
     run(zoo.SEED7_K1, 64, 64, 16)  # tcgen05 fwd / persistent dgrad / wgrad
     run(zoo.IM2COL, 128, 128, 8)
     run(zoo.SEED7_K1, 256, 256, 8, n=1)
+    run(zoo.SEED7_K1, 128, 128, 7)  # K-split small FC (pointwise_ks), padded-quad wgrad
     from paper_2304_07741_b200.dense_conv import TcConv2d
 
     conv = TcConv2d(3, 64, 7, stride=2, padding=3, bias=False).cuda()
