@@ -1309,6 +1309,11 @@ __device__ __forceinline__ void tc_gemm_pix_tmema(const CanvasArgs& a) {
     if constexpr (UNROLL && PW == 8) {
       if (half == 0) produce(IntC<0>{});
       else produce(IntC<1>{});
+    } else if constexpr (UNROLL && PW == 16) {
+      if (half == 0) produce(IntC<0>{});
+      else if (half == 1) produce(IntC<1>{});
+      else if (half == 2) produce(IntC<2>{});
+      else produce(IntC<3>{});
     } else {
       produce(IntC<-1>{});
     }

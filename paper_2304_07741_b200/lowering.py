@@ -2207,7 +2207,7 @@ class Lowerer:
                 tsmem = tstages * 2 * nt * 128 + (2 * tstages + 1) * 8 + 16 + 1024
                 tpw = TC_TMEMA_PW
                 tthreads = (tpw + 2) * 32
-                launcher = f'extern "C" __global__ void __launch_bounds__({tthreads}, {2 if tpair and tpw <= 8 else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_tmema<{name}_F, {nt}, {tstages}, {nacc}, {tpw}, {'true' if K <= TMEMA_UNROLL_MAX and tpw == 8 else 'false'}>(a); }}\n'
+                launcher = f'extern "C" __global__ void __launch_bounds__({tthreads}, {2 if tpair and tpw <= 8 else 1}) {name}(const CanvasArgs a) {{ canvas::tc_gemm_pix_tmema<{name}_F, {nt}, {tstages}, {nacc}, {tpw}, {'true' if K <= TMEMA_UNROLL_MAX and tpw in (8, 16) else 'false'}>(a); }}\n'
                 k = self.add_kernel(name, functor, launcher)
                 pk = self.add_kernel(name + "_pack", "", f'extern "C" __global__ void __launch_bounds__(256) {name}_pack(const CanvasArgs a) {{ canvas::tc_pack_b<{name}_F, {nt}>(a); }}\n')
                 total = nct * kb * nt * 32
