@@ -82,7 +82,7 @@ VEC_PRODUCERS = os.environ.get("CANVAS_VEC", "1") == "1"  # tcgen05 producers ev
 VEC_POINTWISE = os.environ.get("CANVAS_VEC_PW", "1") == "1"  # pointwise launches: 4 consecutive elements per thread
 VEC16 = os.environ.get("CANVAS_VEC16", "1") == "1"  # aligned quads as one 16 B load / store
 VEC_RT = int(os.environ.get("CANVAS_VEC_RT", "0"))  # quads at a run-time 4 B offset: two 16 B loads + select (1: selects, 2: one branch per quad with producer rows grouped by shift class; measured 1.5-2.3x slower on the layer1 GEMMs: off)
-TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares)
+TC_TMEMA_PW = int(os.environ.get("CANVAS_TMEMA_PW", "8"))  # its producer warps (4 lane quadrants x k shares; 16 measured 0.64 vs 0.40 ms on layer1: one CTA per SM)
 TC_TMEMA = os.environ.get("CANVAS_TMEMA", "auto")  # FC forward with the computed operand staged in TMEM (tcgen05.mma A from TMEM): "auto" = when its k loop unrolls fully (K <= TMEMA_UNROLL_MAX), "1" always, "0" never
 TMEMA_STAGES = int(os.environ.get("CANVAS_TMEMA_STAGES", "0"))  # TMEM-A operand stages (0: 3, or 2 when that pairs CTAs)
 TMEMA_UNROLL_MAX = int(os.environ.get("CANVAS_TMEMA_UNROLL_MAX", "1024"))  # fully unrolled TMEM-A producers up to this K (layer1 FC forward 0.656 -> 0.390 ms; without the unroll TMEM-A measured 0.79 ms; at 2304: layer2 K = 1152 0.40 -> 0.54 ms — NT = 128 + 3 A stages > 256 TMEM columns, one CTA per SM — layer3 0.26 -> 0.25)
