@@ -60,6 +60,19 @@ __device__ __forceinline__ float4 win4(const float4 a, const float4 b, const int
 // warp-uniform: the warp-role branches of the tcgen05 templates then stay
 // uniform and producer index math / memory descriptors live on the uniform
 // datapath (measured 2-4% on the layer1 dgrad / wgrad launches)
+// non-coherent loads the compiler may not re-sequence (asm volatile): a functor that
+// issues them first keeps all of them in flight (Lowerer.loads_first, CANVAS_ASM_LOADS)
+__device__ __forceinline__ float ldg_v(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ldg_vp(const float* p, const bool c) {
+  float v = 0.f;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.nc.f32 %0, [%1];\n\t}" : "+f"(v) : "l"(p), "r"((int)c));
+  return v;
+}
+
 __device__ __forceinline__ int warp_index() {
 #ifdef CANVAS_NO_WARP_SHFL
   return threadIdx.x >> 5;

@@ -57,6 +57,8 @@ struct CanvasArgs {
 
 namespace canvas {
 inline float* ptr_add(float* p, int off) { return p + off; }
+inline float ldg_v(const float* p) { return *p; }
+inline float ldg_vp(const float* p, bool c) { return c ? *p : 0.f; }
 template <class F, int V = 1>
 void pointwise(const CanvasArgs& a) {
   for (long long n = 0; n < a.n; ++n)
