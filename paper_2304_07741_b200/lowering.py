@@ -63,7 +63,7 @@ REPLICATE_MIN = 4  # materialise a pointwise node re-evaluated this many times p
 FC_SMALL_W4 = os.environ.get("CANVAS_FC_SMALL_W4", "0") == "1"  # per-pixel small FC: 16 B weight rows (measured slower: 0.080 vs 0.070 ms)
 FC_SMALL_UNROLL = int(os.environ.get("CANVAS_FC_SMALL_UNROLL", "16"))  # per-pixel small FC input-loop unroll (0: Fn.loop default; 16: 0.070 -> 0.068 ms scalar, needed by the quads)
 FC_SMALL_VEC_FILL = int(os.environ.get("CANVAS_FC_SMALL_VEC_FILL", "1024"))  # per-pixel small FC: quads when batch-256 quads >= SMS x this (fc(G) 4x64 at 56^2: 0.070 -> 0.056 ms with unroll 16; at 28^2 quads are slower, 0.081 vs 0.047)
-ASM_LOADS = os.environ.get("CANVAS_ASM_LOADS", "0")  # "1" all, "planes" plane-major launches only, "0" off; loads-first bodies: hoisted gathers as volatile PTX loads (order kept by ptxas); measured mixed, off: grad n1 0.165 -> 0.121 ms at 14^2 but 0.088 -> 0.099 at 7^2 and grad n7 +5% at 14^2 (layer3 -2.5%, layer4 +0.9%, layer1 flat)
+ASM_LOADS = os.environ.get("CANVAS_ASM_LOADS", "planes")  # loads-first bodies: hoisted gathers as volatile PTX loads (order kept by ptxas): "planes" = plane-major launches only (grad n1: layer3 1.385 -> 1.348 ms, layer2 -0.5%, layers 1/4 flat), "1" all (grad n1 at 7x7 0.088 -> 0.099 ms, grad n7 +5% at 14x14), "0" off
 LOADS_FIRST = os.environ.get("CANVAS_LOADS_FIRST", "1") == "1"  # pointwise bodies: gathers hoisted above the arithmetic (grad n1: 0.186 -> 0.165 ms at 14^2, 0.113 -> 0.086 at 7^2, 56^2 unchanged)
 FC_SMALL_KS = os.environ.get("CANVAS_FC_SMALL_KS", "1") == "1"  # per-output small FC with few pixels: K split over lanes
 WGRAD_SMALL_V = os.environ.get("CANVAS_WGRAD_SMALL_V", "1") == "1"  # register-blocked quad wgrad for M <= 16
