@@ -100,7 +100,7 @@ TEXTS = [f"kernel {i}" + ("x" * i) for i in range(12)]
 
 
 def test_all_tasks_complete_in_order():
-    res = CandidateEvaluator([0, 1], fake_ok).run(TEXTS, timeout_s=120)
+    res = CandidateEvaluator([0, 1], fake_ok).run(TEXTS, timeout_s=600)
     assert [r.task_id for r in res] == list(range(12))
     assert all(r.status == "ok" for r in res)
     assert {r.worker for r in res} <= {0, 1}
@@ -109,18 +109,18 @@ def test_all_tasks_complete_in_order():
 
 def test_transient_failure_is_requeued(tmp_path):
     texts = TEXTS[:4] + ["BAD one"]
-    res = CandidateEvaluator([0, 1], fake_flaky, salt=str(tmp_path).replace("/", "_")).run(texts, timeout_s=120)
+    res = CandidateEvaluator([0, 1], fake_flaky, salt=str(tmp_path).replace("/", "_")).run(texts, timeout_s=600)
     assert all(r.status == "ok" for r in res)
 
 
 def test_permanent_failure_reported():
-    res = CandidateEvaluator([0, 1], fake_always_fail).run(TEXTS[:3] + ["BAD kernel"], timeout_s=120)
+    res = CandidateEvaluator([0, 1], fake_always_fail).run(TEXTS[:3] + ["BAD kernel"], timeout_s=600)
     assert [r.status for r in res] == ["ok", "ok", "ok", "failed"]
     assert "does not lower" in res[3].error
 
 
 def test_worker_death_requeues(tmp_path):
-    res = CandidateEvaluator([0, 1], fake_die, salt=str(tmp_path).replace("/", "_")).run(TEXTS[:6] + ["DIE here"] + TEXTS[6:8], timeout_s=120)
+    res = CandidateEvaluator([0, 1], fake_die, salt=str(tmp_path).replace("/", "_")).run(TEXTS[:6] + ["DIE here"] + TEXTS[6:8], timeout_s=600)
     assert len(res) == 9
     # every task completes: the dead worker's held task AND results it had queued
     # but not flushed (tracked in shared memory, released only on arrival)
@@ -133,7 +133,7 @@ def test_compile_ahead_pipeline():
     worker that dies (not just the running one) re-queued."""
     texts = TEXTS[:5] + ["BAD one"] + TEXTS[5:9] + ["DIE here"] + TEXTS[9:]
     salt = str(os.getpid())
-    res = CandidateEvaluator([0, 1], fake_pipelined, prefetch=3, salt=salt).run(texts, timeout_s=120)
+    res = CandidateEvaluator([0, 1], fake_pipelined, prefetch=3, salt=salt).run(texts, timeout_s=600)
     assert [r.task_id for r in res] == list(range(len(texts)))
     st = {texts[r.task_id]: r.status for r in res}
     assert st.pop("BAD one") == "failed"
@@ -143,7 +143,7 @@ def test_compile_ahead_pipeline():
 def test_single_device_survives_worker_crash(tmp_path):
     """One device: a worker that dies is replaced by a fresh process, so the
     sweep still completes (a dead worker used to end a 1-GPU sweep)."""
-    res = CandidateEvaluator([0], fake_die, salt=str(tmp_path).replace("/", "_")).run(TEXTS[:3] + ["DIE here"] + TEXTS[3:6], timeout_s=120)
+    res = CandidateEvaluator([0], fake_die, salt=str(tmp_path).replace("/", "_")).run(TEXTS[:3] + ["DIE here"] + TEXTS[3:6], timeout_s=600)
     assert all(r.status == "ok" for r in res), [(r.task_id, r.status, r.error) for r in res]
 
 
@@ -153,7 +153,7 @@ def test_broken_context_worker_exits_and_is_replaced(monkeypatch):
     (and fails again there), every other task succeeds."""
     monkeypatch.setenv("CANVAS_STICKY_SALT", f"{os.getpid()}-{os.urandom(4).hex()}")  # inherited by the workers
     texts = TEXTS[:3] + ["FAULT kernel"] + TEXTS[3:8]
-    res = CandidateEvaluator([0], fake_sticky, respawns=4).run(texts, timeout_s=120)
+    res = CandidateEvaluator([0], fake_sticky, respawns=4).run(texts, timeout_s=600)
     st = [r.status for r in res]
     assert st[3] == "failed" and "illegal" in res[3].error
     assert st[:3] + st[4:] == ["ok"] * 8, [(r.task_id, r.status, r.error) for r in res]
@@ -161,6 +161,6 @@ def test_broken_context_worker_exits_and_is_replaced(monkeypatch):
 
 def test_parity_checker_injected():
     """The caller's checker decides parity; failures are reported as parity_fail."""
-    res = CandidateEvaluator([0, 1], fake_parity, checker=check_no_odd).run(["k even", "k odd", "k even2"], timeout_s=120)
+    res = CandidateEvaluator([0, 1], fake_parity, checker=check_no_odd).run(["k even", "k odd", "k even2"], timeout_s=600)
     assert [r.status for r in res] == ["ok", "parity_fail", "ok"]
     assert res[1].extra["parity"] == {"ok": False}
