@@ -325,7 +325,17 @@ class CandidateEvaluator:
 
     def run(self, ir_texts, timeout_s: float = 3600.0) -> list[EvalResult]:
         ctx = mp.get_context("spawn")
-        tasks, results = ctx.Queue(), ctx.Queue()
+        # results: a SimpleQueue, whose put writes the pipe synchronously in the worker's
+        # own thread — a worker that exits (os._exit on a broken context, a crash) right
+        # after a put cannot leave a half-flushed message or a held feeder-thread write
+        # lock behind, which with mp.Queue stalls every other worker's reports
+        tasks, results = ctx.Queue(), ctx.SimpleQueue()
+
+        def results_get(timeout: float):
+            if not results._reader.poll(timeout):
+                raise queue.Empty
+            return results.get()
+
         pending = {i: EvalTask(i, t) for i, t in enumerate(ir_texts)}
         for t in pending.values():
             tasks.put(t)
@@ -350,7 +360,7 @@ class CandidateEvaluator:
         try:
             while len(done) < len(pending) and time.monotonic() < deadline:
                 try:
-                    kind, wid, payload = results.get(timeout=0.5)
+                    kind, wid, payload = results_get(0.5)
                 except queue.Empty:
                     # worker lost (process died mid-task): re-queue its task
                     for wid, p in procs.items():
